@@ -1,0 +1,134 @@
+/*
+ * spf.h -- C ABI of libspf.so, the B200 (sm_100a) implementation of the
+ * MInference dynamic sparse pre-fill path (online estimation -> index
+ * compaction -> sparse FlashAttention).
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; every tensor pointer is a DEVICE pointer
+ *     unless the parameter name ends in `_host`;
+ *   - tensors are dense row-major: Q [n_q_heads][seq_len][head_dim],
+ *     K/V [n_kv_heads][seq_len][head_dim]; q-head h reads kv-head
+ *     h / (n_q_heads / n_kv_heads) (GQA);
+ *   - per-(head, query-block-row) layouts are CSR: row index = h*n_rows + r,
+ *     n_rows = ceil(seq_len / block_size), offsets are int64 [n_q_heads*n_rows + 1],
+ *     entries int32 (tile starts / column indices, as in kernels.py:28-35 but
+ *     with 32-bit entries);
+ *   - work is enqueued on `stream` (a cudaStream_t; NULL = legacy default);
+ *     functions return 0 on success, a non-zero SPF_ERR_* code otherwise,
+ *     and spf_last_error() describes the failure (thread-local string);
+ *   - nothing here allocates device memory: callers pass workspaces sized by
+ *     the matching *_workspace_size() query.
+ *
+ * The reference interface each entry point replaces is cited inline
+ * (paths relative to /root/reference/pkg/src/sparseprefill/).
+ */
+#ifndef SPF_H_
+#define SPF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPF_OK 0
+#define SPF_ERR_CUDA 1
+#define SPF_ERR_INVALID 2
+#define SPF_ERR_CAPACITY 3
+
+#define SPF_DTYPE_BF16 0
+#define SPF_DTYPE_F32 1
+
+/* Library identification / error reporting. */
+int spf_version(void);
+const char* spf_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Sparse FlashAttention forward.
+ * Replaces the kernel plugin call kernels.py:60-70 -> _core.sparse_flash_rows
+ * (_core.pyx:72-192): streaming softmax over each query-block row's tiles
+ * (keys [max(s,0), min(s+B,S)), per-cell causal) and then its residual
+ * columns in chips of B (allowed = leading columns <= query); rows with no
+ * coverage produce zeros.  Batched over heads with a GQA head map.
+ *   dtype   : SPF_DTYPE_BF16 (bf16 in/out, the production path) or
+ *             SPF_DTYPE_F32 (fp32 in/out via bf16x2 split, the drop-in path)
+ *   out     : [n_q_heads][seq_len][head_dim] of the same dtype
+ *   head_dim: <= 128 (padded internally to 64/128 through the workspace)
+ * ------------------------------------------------------------------------- */
+size_t spf_sparse_flash_workspace_size(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim);
+int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
+                          int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
+                          const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
+                          void* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Vertical-Slash online estimation.
+ * Replaces estimator.py:82-114 (estimate_vertical_slash): probabilities of
+ * the last `last_q` query rows against all keys (scale 1/sqrt(head_dim),
+ * causal), rounded to fp32, summed per column (vertical) and per diagonal
+ * offset (slash) in fp64, then top-k with ties to the lower index and index 0
+ * force-included (estimator.py:59-79).
+ *   vertical_out : [n_q_heads][k_v_eff] int32, ascending   (k_v_eff = min(k_v, S))
+ *   slash_out    : [n_q_heads][k_s_eff] int32, descending  (k_s_eff = min(k_s, S))
+ *   vscore_out / sscore_out : optional [n_q_heads][seq_len] fp64 score vectors
+ *                  (may be NULL; used for parity tests)
+ * ------------------------------------------------------------------------- */
+size_t spf_vs_estimate_workspace_size(int n_q_heads, int seq_len, int last_q);
+int spf_vs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+                    int head_dim, int last_q, int k_v, int k_s, int32_t* vertical_out, int32_t* slash_out,
+                    double* vscore_out, double* sscore_out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Block-Sparse online estimation.
+ * Replaces estimator.py:117-143 (estimate_block_sparse) with tensor.py:43-58
+ * pooling: fp64 block means rounded to fp32, fp64 pooled scores,
+ * block-causal softmax rounded to fp32, per row top-min(k_b, r+1) with the
+ * diagonal forced, ascending.  Output is directly the CSR tile layout of
+ * sparse_attn.py:30-33 (tile start = block * block_size):
+ *   tile_starts_out  : [n_q_heads * sum_r min(k_b, r+1)] int32
+ *   tile_offsets_out : [n_q_heads * n_rows + 1] int64
+ * ------------------------------------------------------------------------- */
+size_t spf_bs_estimate_workspace_size(int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int block_size);
+int spf_bs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+                    int head_dim, int k_b, int block_size, int32_t* tile_starts_out, int64_t* tile_offsets_out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Index compaction (two-phase: count, then fill into caller-sized CSR).
+ * Vertical-Slash point-range merge, vs_index.py:28-95 (Alg. 4), bit-exact:
+ *   vertical [n_heads][n_v] ascending, slash [n_heads][n_s] descending.
+ * spf_vs_layout_count writes tile_offsets/col_offsets ([n_heads*n_rows+1],
+ * exclusive prefix sums) and the two totals to totals_host[2] (synchronises
+ * `stream`).  spf_vs_layout_fill writes the entries.
+ * ------------------------------------------------------------------------- */
+size_t spf_layout_workspace_size(int n_heads, int seq_len, int block_size);
+int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, int n_heads,
+                        int seq_len, int block_size, int64_t* tile_offsets, int64_t* col_offsets,
+                        int64_t* totals_host, void* workspace, size_t workspace_bytes, void* stream);
+int spf_vs_layout_fill(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, int n_heads, int seq_len,
+                       int block_size, const int64_t* tile_offsets, const int64_t* col_offsets,
+                       int32_t* tile_starts, int32_t* col_indices, void* stream);
+
+/* A-shape static layout, patterns.py:109-128 (sink tiles + aligned local
+ * window per row).  Same two-phase contract (no columns). */
+int spf_ashape_layout_count(int n_heads, int seq_len, int block_size, int global_tokens, int local_window,
+                            int64_t* tile_offsets, int64_t* totals_host, void* workspace, size_t workspace_bytes,
+                            void* stream);
+int spf_ashape_layout_fill(int n_heads, int seq_len, int block_size, int global_tokens, int local_window,
+                           const int64_t* tile_offsets, int32_t* tile_starts, void* stream);
+
+/* Computed cells at kernel granularity (patterns.py:147-184, layout_area):
+ * area_out[n_heads] int64.  Used for kernel_sparsity and FLOP accounting. */
+int spf_layout_area(int n_heads, int seq_len, int block_size, const int32_t* tile_starts,
+                    const int64_t* tile_offsets, const int64_t* col_offsets, int64_t* area_out, void* stream);
+
+/* Round/convert helper for callers holding fp32 data that want the bf16
+ * production path: dst[i] = bf16_rn(src[i]). */
+int spf_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPF_H_ */

@@ -1,0 +1,36 @@
+// spf_internal.h -- host-side declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace spf {
+
+// Sets the thread-local last-error string and returns the status code.
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+
+// Encodes a 3-D [dim2][dim1][dim0] bf16 tensor map with a (64 x rows x 1) box
+// and 128-byte swizzle; used for every Q/K/V operand.
+int make_tmap_bf16_3d(CUtensorMap* map, const void* base, int dim0, int dim1, int dim2, int box_rows);
+
+struct AttnArgs {
+  int S, Hq, Hkv, B, d_out;
+  float scale;
+  const int32_t* tile_starts;
+  const int64_t* tile_offsets;
+  const int32_t* col_indices;
+  const int64_t* col_offsets;
+  // bf16 operands, padded to kD (64 or 128); *_lo are the split residuals (fp32 I/O path)
+  const void *q_hi, *k_hi, *v_hi, *q_lo, *k_lo, *v_lo;
+  void* out;
+  bool out_f32;
+  int kD;
+  bool split;
+  const int32_t* work_order;  // optional: CTA -> work-item permutation (nullptr = heavy rows first)
+};
+
+int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
+
+}  // namespace spf

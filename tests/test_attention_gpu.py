@@ -1,0 +1,144 @@
+"""Parity of the sm_100a sparse FlashAttention kernel (libspf) against the
+reference kernel contract (_core.pyx:72-192) restated in oracle/port.py and
+against the reference's own outputs stored in tests/golden.
+
+Tolerances (BASELINE.json north_star): fp32 I/O -> max-abs error <= 1e-3 x
+max(1, max|ref|) ("1e-3 relative"); bf16 I/O -> max-abs <= 2e-2.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bf16_round, gaussian_qkv
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-3
+BF16_TOL = 2e-2
+
+
+def rel_err(got, want):
+    return float(np.max(np.abs(got.astype(np.float64) - want.astype(np.float64)))) / max(
+        1.0, float(np.max(np.abs(want))))
+
+
+def max_abs(got, want):
+    return float(np.max(np.abs(got.astype(np.float64) - want.astype(np.float64))))
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2407_02490_b200 import kernels
+
+    return kernels
+
+
+def _rows_of(blocks, s, b):
+    return np.concatenate([np.arange(r * b, min(r * b + b, s)) for r in blocks])
+
+
+@pytest.mark.parametrize("prefix", ["vs_", "bs_", "as_"])
+def test_golden_layouts_fp32(golden, K, prefix):
+    names = sorted({k.split("__")[0] for k in golden.files if k.startswith(prefix)})
+    assert names
+    for name in names:
+        prm = golden[f"{name}__params"]
+        if prefix == "vs_":
+            s, d, _, _, _, seed, bf16, b = (int(x) for x in prm)
+            cols, col_off = golden[f"{name}__cols"], golden[f"{name}__col_off"]
+        elif prefix == "bs_":
+            s, d, _, b, seed, bf16 = (int(x) for x in prm)
+        else:
+            s, d, _, _, b, seed, bf16 = (int(x) for x in prm)
+        if prefix != "vs_":
+            n = (s + b - 1) // b
+            cols, col_off = np.zeros(0, np.int64), np.zeros(n + 1, np.int64)
+        q, k, v = gaussian_qkv(s, d, seed, bool(bf16))
+        got = K.sparse_flash_rows(q, k, v, 1.0 / math.sqrt(d), b, golden[f"{name}__tiles"],
+                                  golden[f"{name}__tile_off"], cols, col_off)
+        rows = _rows_of(golden[f"{name}__out_blocks"], s, b)
+        err = rel_err(got[rows], golden[f"{name}__out"])
+        assert err <= F32_TOL, (name, err)
+
+
+def _random_layout(rng, s, b, n_tiles=3, n_cols=5, unaligned=True):
+    n = (s + b - 1) // b
+    tiles, cols = [], []
+    for r in range(n):
+        q_end = min((r + 1) * b, s)
+        if unaligned:
+            cand = np.sort(rng.choice(np.arange(-b // 2, q_end), size=min(n_tiles, q_end + b // 2), replace=False))
+        else:
+            cand = np.arange(0, q_end, b)
+            cand = np.sort(rng.choice(cand, size=min(n_tiles, cand.size), replace=False))
+        tiles.append([int(x) for x in cand])
+        cc = np.sort(rng.choice(q_end, size=min(n_cols, q_end), replace=False))
+        cols.append([int(x) for x in cc])
+    return tiles, cols
+
+
+@pytest.mark.parametrize("s,d,b", [(17, 16, 4), (64, 16, 16), (257, 64, 64), (300, 128, 64), (1000, 128, 64),
+                                   (515, 32, 16), (200, 64, 100), (130, 128, 2), (777, 128, 128)])
+def test_random_layouts_fp32(K, s, d, b):
+    rng = np.random.Generator(np.random.PCG64(1000 * s + d + b))
+    q, k, v = gaussian_qkv(s, d, s + d)
+    tiles, cols = _random_layout(rng, s, b)
+    ts, to = port.flatten(tiles)
+    cs, co = port.flatten(cols)
+    want = port.sparse_flash_rows(q, k, v, 1.0 / math.sqrt(d), b, ts, to, cs, co)
+    got = K.sparse_flash_attention(q, k, v, 1.0 / math.sqrt(d), b, tiles, cols)
+    assert rel_err(got, want) <= F32_TOL
+
+
+def test_empty_rows_zero_and_full_equals_dense(K):
+    # test_sparse_attn.py:58-85 of the reference
+    q, k, v = gaussian_qkv(8, 4, 3)
+    out = K.sparse_flash_attention(q, k, v, 0.5, 4, [[], [4]], [[], []])
+    np.testing.assert_array_equal(out[:4], np.zeros((4, 4)))
+    assert np.any(out[4:] != 0)
+    q, k, v = gaussian_qkv(50, 8, 4)
+    tiles, cols, _ = port.build_vs_layout_with_stats([0], list(range(49, -1, -1)), 50, 8)
+    got = K.sparse_flash_attention(q, k, v, 1 / math.sqrt(8), 8, tiles, cols)
+    mask = np.tril(np.ones((50, 50), bool))
+    want = port.masked_attention(q, k, v, 1 / math.sqrt(8), mask)
+    assert rel_err(got, want) <= F32_TOL
+
+
+def test_row_count_mismatch_rejected(K):
+    q, k, v = gaussian_qkv(16, 4, 0)
+    with pytest.raises(ValueError):
+        K.sparse_flash_attention(q, k, v, 0.5, 4, [[0]], [[]])
+
+
+@pytest.mark.parametrize("s,hq,hkv,b", [(1000, 4, 2, 64), (4096, 8, 2, 64), (2048, 4, 4, 32)])
+def test_multihead_bf16_gqa(K, s, hq, hkv, b):
+    d = 128
+    rng = np.random.Generator(np.random.PCG64(s + hq))
+    q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    v = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    n = (s + b - 1) // b
+    tiles_all, cols_all = [], []
+    for h in range(hq):
+        t, c = _random_layout(rng, s, b, n_tiles=6, n_cols=40)
+        tiles_all += t
+        cols_all += c
+    ts, to = port.flatten(tiles_all)
+    cs, co = port.flatten(cols_all)
+    dev = torch.device("cuda")
+    out = K.sparse_flash_attention_gpu(
+        torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+        torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+        torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+        torch.from_numpy(cs.astype(np.int32)).to(dev), torch.from_numpy(co).to(dev)).float().cpu().numpy()
+    worst = 0.0
+    for h in range(hq):
+        kvh = h // (hq // hkv)
+        sl = slice(h * n, (h + 1) * n + 1)
+        want = port.sparse_flash_rows(q[h], k[kvh], v[kvh], 1 / math.sqrt(d), b, ts, to[sl], cs, co[sl])
+        worst = max(worst, max_abs(out[h], want))
+    assert worst <= BF16_TOL, worst

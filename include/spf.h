@@ -62,65 +62,81 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
                           const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
                           void* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Heads selection: the estimation and layout entry points below work on a
+ * subset of q-heads given by `head_ids` (device int32 [n_heads]; NULL means
+ * heads 0..n_heads-1) so a layer whose heads use different patterns fills
+ * one CSR over all n_q_heads (rows of other heads are left untouched).
+ */
+
 /* ---------------------------------------------------------------------------
  * Vertical-Slash online estimation.
  * Replaces estimator.py:82-114 (estimate_vertical_slash): probabilities of
  * the last `last_q` query rows against all keys (scale 1/sqrt(head_dim),
- * causal), rounded to fp32, summed per column (vertical) and per diagonal
- * offset (slash) in fp64, then top-k with ties to the lower index and index 0
+ * causal), computed from fp64 scores and rounded to fp32 (tensor.py:78),
+ * summed per column (vertical) and per diagonal offset (slash) in fp64 in the
+ * reference's order, then top-k with ties to the lower index and index 0
  * force-included (estimator.py:59-79).
- *   vertical_out : [n_q_heads][k_v_eff] int32, ascending   (k_v_eff = min(k_v, S))
- *   slash_out    : [n_q_heads][k_s_eff] int32, descending  (k_s_eff = min(k_s, S))
- *   vscore_out / sscore_out : optional [n_q_heads][seq_len] fp64 score vectors
+ *   vertical_out : [n_heads][min(k_v, S)] int32, ascending
+ *   slash_out    : [n_heads][min(k_s, S)] int32, descending
+ *   vscore_out / sscore_out : optional [n_heads][seq_len] fp64 score vectors
  *                  (may be NULL; used for parity tests)
  * ------------------------------------------------------------------------- */
-size_t spf_vs_estimate_workspace_size(int n_q_heads, int seq_len, int last_q);
+size_t spf_vs_estimate_workspace_size(int n_heads, int seq_len, int last_q);
 int spf_vs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
-                    int head_dim, int last_q, int k_v, int k_s, int32_t* vertical_out, int32_t* slash_out,
-                    double* vscore_out, double* sscore_out, void* workspace, size_t workspace_bytes,
-                    void* stream);
+                    int head_dim, const int32_t* head_ids, int n_heads, int last_q, int k_v, int k_s,
+                    int32_t* vertical_out, int32_t* slash_out, double* vscore_out, double* sscore_out,
+                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Block-Sparse online estimation.
  * Replaces estimator.py:117-143 (estimate_block_sparse) with tensor.py:43-58
  * pooling: fp64 block means rounded to fp32, fp64 pooled scores,
  * block-causal softmax rounded to fp32, per row top-min(k_b, r+1) with the
- * diagonal forced, ascending.  Output is directly the CSR tile layout of
- * sparse_attn.py:30-33 (tile start = block * block_size):
- *   tile_starts_out  : [n_q_heads * sum_r min(k_b, r+1)] int32
- *   tile_offsets_out : [n_q_heads * n_rows + 1] int64
+ * diagonal forced, ascending.  The result is written straight into the CSR
+ * tile layout of sparse_attn.py:30-33 (tile start = block * block_size) at
+ * rows head_ids[i]*n_rows + r, using tile_offsets produced by
+ * spf_bs_layout_count + spf_csr_offsets.
  * ------------------------------------------------------------------------- */
 size_t spf_bs_estimate_workspace_size(int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int block_size);
 int spf_bs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
-                    int head_dim, int k_b, int block_size, int32_t* tile_starts_out, int64_t* tile_offsets_out,
-                    void* workspace, size_t workspace_bytes, void* stream);
+                    int head_dim, const int32_t* head_ids, int n_heads, int k_b, int block_size,
+                    const int64_t* tile_offsets, int32_t* tile_starts, void* workspace, size_t workspace_bytes,
+                    void* stream);
 
 /* ---------------------------------------------------------------------------
- * Index compaction (two-phase: count, then fill into caller-sized CSR).
- * Vertical-Slash point-range merge, vs_index.py:28-95 (Alg. 4), bit-exact:
- *   vertical [n_heads][n_v] ascending, slash [n_heads][n_s] descending.
- * spf_vs_layout_count writes tile_offsets/col_offsets ([n_heads*n_rows+1],
- * exclusive prefix sums) and the two totals to totals_host[2] (synchronises
- * `stream`).  spf_vs_layout_fill writes the entries.
+ * Index compaction.  Three steps: per-row counts (per pattern, into
+ * int64 [n_q_heads*n_rows] count arrays), one scan (spf_csr_offsets), then
+ * per-pattern fills.
  * ------------------------------------------------------------------------- */
-size_t spf_layout_workspace_size(int n_heads, int seq_len, int block_size);
-int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, int n_heads,
-                        int seq_len, int block_size, int64_t* tile_offsets, int64_t* col_offsets,
-                        int64_t* totals_host, void* workspace, size_t workspace_bytes, void* stream);
-int spf_vs_layout_fill(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, int n_heads, int seq_len,
-                       int block_size, const int64_t* tile_offsets, const int64_t* col_offsets,
-                       int32_t* tile_starts, int32_t* col_indices, void* stream);
+size_t spf_scan_workspace_size(int64_t n);
+/* offsets[0] = 0, offsets[i+1] = sum(counts[0..i]); the total is copied to
+ * *total_host (synchronising `stream`) when total_host != NULL. */
+int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t* total_host, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* Vertical-Slash point-range merge, vs_index.py:28-95 (Alg. 4), bit-exact.
+ * vertical [n_heads][n_v] ascending, slash [n_heads][n_s] descending. */
+int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, const int32_t* head_ids,
+                        int n_heads, int seq_len, int block_size, int64_t* tile_counts, int64_t* col_counts,
+                        void* stream);
+int spf_vs_layout_fill(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, const int32_t* head_ids,
+                       int n_heads, int seq_len, int block_size, const int64_t* tile_offsets,
+                       const int64_t* col_offsets, int32_t* tile_starts, int32_t* col_indices, void* stream);
 
 /* A-shape static layout, patterns.py:109-128 (sink tiles + aligned local
- * window per row).  Same two-phase contract (no columns). */
-int spf_ashape_layout_count(int n_heads, int seq_len, int block_size, int global_tokens, int local_window,
-                            int64_t* tile_offsets, int64_t* totals_host, void* workspace, size_t workspace_bytes,
-                            void* stream);
-int spf_ashape_layout_fill(int n_heads, int seq_len, int block_size, int global_tokens, int local_window,
-                           const int64_t* tile_offsets, int32_t* tile_starts, void* stream);
+ * window per row, no columns). */
+int spf_ashape_layout_count(const int32_t* head_ids, int n_heads, int seq_len, int block_size, int global_tokens,
+                            int local_window, int64_t* tile_counts, void* stream);
+int spf_ashape_layout_fill(const int32_t* head_ids, int n_heads, int seq_len, int block_size, int global_tokens,
+                           int local_window, const int64_t* tile_offsets, int32_t* tile_starts, void* stream);
 
-/* Computed cells at kernel granularity (patterns.py:147-184, layout_area):
- * area_out[n_heads] int64.  Used for kernel_sparsity and FLOP accounting. */
+/* Block-Sparse row counts min(k_b, r+1) (estimator.py:139-142). */
+int spf_bs_layout_count(const int32_t* head_ids, int n_heads, int seq_len, int block_size, int k_b,
+                        int64_t* tile_counts, void* stream);
+
+/* Computed cells at kernel granularity (patterns.py:147-184, layout_area)
+ * for every head of a CSR layout: area_out[n_heads] int64.  Used for
+ * kernel_sparsity (metrics.py:43-45) and FLOP accounting. */
 int spf_layout_area(int n_heads, int seq_len, int block_size, const int32_t* tile_starts,
                     const int64_t* tile_offsets, const int64_t* col_offsets, int64_t* area_out, void* stream);
 

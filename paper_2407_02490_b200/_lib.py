@@ -30,17 +30,19 @@ SIGNATURES = {
     "spf_sparse_flash_rows": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
                                        _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "spf_vs_estimate_workspace_size": (_c_size, [_c_int, _c_int, _c_int]),
-    "spf_vs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
-                                 _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "spf_vs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
+                                 _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "spf_bs_estimate_workspace_size": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int]),
-    "spf_bs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
-                                 _vp, _c_size, _vp]),
-    "spf_layout_workspace_size": (_c_size, [_c_int, _c_int, _c_int]),
-    "spf_vs_layout_count": (_c_int, [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_size,
-                                     _vp]),
-    "spf_vs_layout_fill": (_c_int, [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
-    "spf_ashape_layout_count": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_size, _vp]),
-    "spf_ashape_layout_fill": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "spf_bs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
+                                 _vp, _vp, _vp, _c_size, _vp]),
+    "spf_scan_workspace_size": (_c_size, [_i64]),
+    "spf_csr_offsets": (_c_int, [_vp, _i64, _vp, _vp, _vp, _c_size, _vp]),
+    "spf_vs_layout_count": (_c_int, [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "spf_vs_layout_fill": (_c_int, [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
+                                    _vp]),
+    "spf_ashape_layout_count": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "spf_ashape_layout_fill": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "spf_bs_layout_count": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "spf_layout_area": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
     "spf_f32_to_bf16": (_c_int, [_vp, _vp, _i64, _vp]),
 }

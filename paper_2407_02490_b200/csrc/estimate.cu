@@ -1,0 +1,421 @@
+// estimate.cu -- online sparse-index estimation on the GPU.
+//
+// Vertical-Slash, estimator.py:82-114 (rounding points of tensor.py:61-78):
+//   1. score pass   s[i][j] = scale * (q_tail[i] . k[j]) in fp64 (exact-enough:
+//                   bf16/fp32 inputs, fp64 FMA chain), masked j > abs_i, plus
+//                   per-(row, 64-key block) partial (max, sum exp);
+//   2. row stats    m_i, l_i combined from the partials (fixed tree order);
+//   3. vertical     p[i][j] = fp32(exp(s - m_i) / l_i) (the reference's fp32
+//                   rounding point), vertical[j] = sum_i p (fp64, i ascending,
+//                   est.sum(axis=0));
+//   4. slash        slash[o] = sum_i p[i][abs_i - o] (fp64, i ascending, the
+//                   np.bincount order);
+//   5. top-k        block radix select, lowest index wins ties, index 0 forced.
+// Block-Sparse, estimator.py:117-143:
+//   1. pooling      fp64 block sums / real length -> fp32 (tensor.py:43-58);
+//   2. score pass   pooled scores in fp64 for the causal block triangle;
+//   3. row pass     block-causal softmax -> fp32, top-min(k_b, r+1) with the
+//                   diagonal forced, written straight into the CSR tile layout
+//                   (tile start = block * B, sparse_attn.py:30-33).
+// fp64 is used for every score so the fp32-rounded probabilities -- and hence
+// the selected index sets -- are those of the reference.
+#include <cuda_bf16.h>
+
+#include "spf.h"
+#include "spf_internal.h"
+#include "topk.cuh"
+
+namespace spf {
+namespace {
+
+constexpr int kTile = 64;       // rows x keys per score tile
+constexpr int kScoreThreads = 256;
+constexpr int kLd = kTile + 2;  // padded smem leading dimension (doubles)
+
+template <typename T>
+__device__ __forceinline__ double ld_as_double(const T* p) {
+  return static_cast<double>(static_cast<float>(*p));
+}
+template <>
+__device__ __forceinline__ double ld_as_double<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return static_cast<double>(__bfloat162float(*p));
+}
+
+// Generic fp64 tile: C[a, b] = scale * A[a] . B[b] for a 64x64 tile.
+//   VS mode: A = q tail rows, abs row = a_abs0 + a; mask b > abs row; emits partial stats.
+//   BS mode: A = pooled q rows (row index = block r), B = pooled k rows; skips tiles above the diagonal.
+template <typename TA, typename TB, bool kVS>
+__global__ void __launch_bounds__(kScoreThreads) score_tile_kernel(
+    const TA* __restrict__ A, const TB* __restrict__ Bm, const int32_t* __restrict__ head_ids, int heads_per_kv,
+    int64_t a_head_stride, int64_t b_head_stride, int a_row0, int n_a, int n_b, int d, double scale, int a_abs0,
+    double* __restrict__ out, int64_t out_head_stride, double2* __restrict__ stats, int n_kblk) {
+  extern __shared__ double smd[];
+  double* At = smd;               // [d][kLd]
+  double* Bt = smd + d * kLd;     // [d][kLd]
+  const int hi = blockIdx.z;
+  const int h = head_ids ? head_ids[hi] : hi;
+  const int kvh = h / heads_per_kv;
+  const int bt = blockIdx.x, at = blockIdx.y;
+  if (!kVS && bt > at) return;  // BS: block-causal triangle only
+  const int a0 = at * kTile, b0 = bt * kTile;
+  const TA* Ah = A + (int64_t)h * a_head_stride + (int64_t)a_row0 * d;
+  const TB* Bh = Bm + (int64_t)kvh * b_head_stride;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kTile * d; e += kScoreThreads) {
+    const int r = e / d, c = e % d;
+    At[c * kLd + r] = (a0 + r < n_a) ? ld_as_double(Ah + (int64_t)(a0 + r) * d + c) : 0.0;
+    Bt[c * kLd + r] = (b0 + r < n_b) ? ld_as_double(Bh + (int64_t)(b0 + r) * d + c) : 0.0;
+  }
+  __syncthreads();
+  const int tr = tid >> 4, tk = tid & 15;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double2 qa = *reinterpret_cast<const double2*>(At + c * kLd + 4 * tr);
+    const double2 qb = *reinterpret_cast<const double2*>(At + c * kLd + 4 * tr + 2);
+    const double2 ka = *reinterpret_cast<const double2*>(Bt + c * kLd + 4 * tk);
+    const double2 kb = *reinterpret_cast<const double2*>(Bt + c * kLd + 4 * tk + 2);
+    const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
+    const double kv[4] = {ka.x, ka.y, kb.x, kb.y};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(qv[i], kv[j], acc[i][j]);
+  }
+  double* outh = out + (int64_t)hi * out_head_stride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = a0 + 4 * tr + i;
+    double s[4];
+    double mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int b = b0 + 4 * tk + j;
+      s[j] = scale * acc[i][j];
+      const bool valid = (a < n_a) && (b < n_b) && (kVS ? (b <= a_abs0 + a) : (b <= a));
+      if (valid) mx = fmax(mx, s[j]);
+      else s[j] = -INFINITY;
+    }
+    if (a < n_a) {
+      double* orow = outh + (int64_t)a * n_b + b0 + 4 * tk;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (b0 + 4 * tk + j < n_b) orow[j] = s[j];
+    }
+    if (kVS) {
+      // partial (max, sum exp) over this tile's 64 keys, fixed butterfly order
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double l = 0.0;
+      if (mx != -INFINITY) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (s[j] != -INFINITY) l += exp(s[j] - mx);
+      }
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      if (tk == 0 && a < n_a) stats[((int64_t)hi * n_a + a) * n_kblk + bt] = make_double2(mx, l);
+    }
+  }
+}
+
+// One warp per (head, tail row): combine the partial stats (fixed order).
+__global__ void vs_rowstats_kernel(const double2* __restrict__ stats, int n_rows_total, int n_kblk,
+                                   double2* __restrict__ row_ml) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_rows_total) return;
+  const double2* st = stats + (int64_t)w * n_kblk;
+  double m = -INFINITY, l = 0.0;
+  for (int b = lane; b < n_kblk; b += 32) {
+    const double2 v = st[b];
+    if (v.x == -INFINITY) continue;
+    if (v.x > m) {
+      l = l * exp(m - v.x) + v.y;
+      m = v.x;
+    } else {
+      l += v.y * exp(v.x - m);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const double l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    const double mn = fmax(m, m2);
+    double ln = 0.0;
+    if (mn != -INFINITY) ln = (m == -INFINITY ? 0.0 : l * exp(m - mn)) + (m2 == -INFINITY ? 0.0 : l2 * exp(m2 - mn));
+    m = mn;
+    l = ln;
+  }
+  if (lane == 0) row_ml[w] = make_double2(m, l);
+}
+
+// p = fp32(exp(s - m)/l); vertical[j] = sum_i p (i ascending); p kept for the slash pass.
+__global__ void vs_vertical_kernel(const double* __restrict__ s, const double2* __restrict__ row_ml, int L, int S,
+                                   float* __restrict__ p, double* __restrict__ vertical) {
+  const int hi = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const double* sh = s + (int64_t)hi * L * S;
+  float* ph = p + (int64_t)hi * L * S;
+  const double2* ml = row_ml + (int64_t)hi * L;
+  double acc = 0.0;
+  for (int i = 0; i < L; ++i) {
+    const int abs_i = S - L + i;
+    float pv = 0.f;
+    if (j <= abs_i) {
+      const double2 st = ml[i];
+      pv = __double2float_rn(exp(sh[(int64_t)i * S + j] - st.x) / st.y);
+    }
+    ph[(int64_t)i * S + j] = pv;
+    acc += (double)pv;
+  }
+  vertical[(int64_t)hi * S + j] = acc;
+}
+
+__global__ void vs_slash_kernel(const float* __restrict__ p, int L, int S, double* __restrict__ slash) {
+  const int hi = blockIdx.y;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= S) return;
+  const float* ph = p + (int64_t)hi * L * S;
+  double acc = 0.0;
+  for (int i = 0; i < L; ++i) {
+    const int j = S - L + i - o;
+    if (j >= 0) acc += (double)ph[(int64_t)i * S + j];
+  }
+  slash[(int64_t)hi * S + o] = acc;
+}
+
+constexpr int kTopkThreads = 1024;
+
+__global__ void __launch_bounds__(kTopkThreads) vs_topk_kernel(const double* __restrict__ vscore,
+                                                               const double* __restrict__ sscore, int S, int k_v,
+                                                               int k_s, int32_t* __restrict__ vert_out,
+                                                               int32_t* __restrict__ slash_out) {
+  using TK = BlockTopK<kTopkThreads, double>;
+  __shared__ typename TK::Storage sm;
+  const int hi = blockIdx.x;
+  if (blockIdx.y == 0)
+    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, 0, false, vert_out + (int64_t)hi * k_v, 1);
+  else
+    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, 0, true, slash_out + (int64_t)hi * k_s, 1);
+}
+
+// ---------------------------------------------------------------- Block-Sparse
+template <typename T>
+__global__ void pool_kernel(const T* __restrict__ x, int64_t n_rows_total, int S, int d, int B,
+                            float* __restrict__ pooled) {
+  // one thread per (head-row-block, column): fp64 sequential sum / real length -> fp32
+  const int n_blk = (S + B - 1) / B;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = n_rows_total * (int64_t)n_blk * d;  // n_rows_total = number of heads
+  if (idx >= total) return;
+  const int c = (int)(idx % d);
+  const int64_t hb = idx / d;
+  const int64_t h = hb / n_blk;
+  const int r = (int)(hb % n_blk);
+  const int r0 = r * B, r1 = min(r0 + B, S);
+  const T* base = x + (h * S + r0) * (int64_t)d + c;
+  double acc = 0.0;
+  for (int i = 0; i < r1 - r0; ++i) acc += ld_as_double(base + (int64_t)i * d);
+  pooled[idx] = __double2float_rn(acc / (double)(r1 - r0));
+}
+
+constexpr int kBsThreads = 256;
+
+// One CTA per (head, block row r): block-causal softmax of the pooled scores
+// (fp64, rounded to fp32), top-min(k_b, r+1) with the diagonal forced.
+__global__ void __launch_bounds__(kBsThreads) bs_row_kernel(const double* __restrict__ scores, int N, int k_b, int B,
+                                                            const int32_t* __restrict__ head_ids,
+                                                            const int64_t* __restrict__ tile_offsets,
+                                                            int32_t* __restrict__ tile_starts) {
+  using TK = BlockTopK<kBsThreads, float>;
+  __shared__ typename TK::Storage sm;
+  __shared__ double red[kBsThreads / 32];
+  extern __shared__ float pv[];  // [N]
+  const int hi = blockIdx.y;
+  const int h = head_ids ? head_ids[hi] : hi;
+  const int r = blockIdx.x;
+  const int n = r + 1;
+  const double* sr = scores + ((int64_t)hi * N + r) * N;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // row max (exact)
+  double m = -INFINITY;
+  for (int b = tid; b < n; b += kBsThreads) m = fmax(m, sr[b]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[wid] = m;
+  __syncthreads();
+  m = red[0];
+  for (int w = 1; w < kBsThreads / 32; ++w) m = fmax(m, red[w]);
+  __syncthreads();
+  // denominator (fixed tree order)
+  double l = 0.0;
+  for (int b = tid; b < n; b += kBsThreads) l += exp(sr[b] - m);
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) red[wid] = l;
+  __syncthreads();
+  l = 0.0;
+  for (int w = 0; w < kBsThreads / 32; ++w) l += red[w];
+  for (int b = tid; b < n; b += kBsThreads) pv[b] = __double2float_rn(exp(sr[b] - m) / l);
+  __syncthreads();
+  const int64_t row = (int64_t)h * N + r;
+  TK::run(sm, pv, n, min(k_b, n), r, false, tile_starts + tile_offsets[row], B);
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+template <typename T>
+int vs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids, int n_heads,
+                     int L, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
+                     uint8_t* ws, cudaStream_t st) {
+  const int n_kblk = (S + kTile - 1) / kTile;
+  double* s = reinterpret_cast<double*>(ws);
+  ws += align256((size_t)n_heads * L * S * 8);
+  float* p = reinterpret_cast<float*>(ws);
+  ws += align256((size_t)n_heads * L * S * 4);
+  double2* stats = reinterpret_cast<double2*>(ws);
+  ws += align256((size_t)n_heads * L * n_kblk * 16);
+  double2* row_ml = reinterpret_cast<double2*>(ws);
+  ws += align256((size_t)n_heads * L * 16);
+  if (vscore == nullptr) {
+    vscore = reinterpret_cast<double*>(ws);
+    ws += align256((size_t)n_heads * S * 8);
+  }
+  if (sscore == nullptr) {
+    sscore = reinterpret_cast<double*>(ws);
+    ws += align256((size_t)n_heads * S * 8);
+  }
+  const size_t smem = (size_t)2 * d * kLd * sizeof(double);
+  auto kern = score_tile_kernel<T, T, true>;
+  int rc;
+  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "score smem attr")))
+    return rc;
+  dim3 grid((unsigned)n_kblk, (unsigned)((L + kTile - 1) / kTile), (unsigned)n_heads);
+  kern<<<grid, kScoreThreads, smem, st>>>(q, k, head_ids, Hq / Hkv, (int64_t)S * d, (int64_t)S * d, S - L, L, S, d,
+                                          1.0 / sqrt((double)d), S - L, s, (int64_t)L * S, stats, n_kblk);
+  if ((rc = check_cuda(cudaGetLastError(), "vs score"))) return rc;
+  const int rows_total = n_heads * L;
+  vs_rowstats_kernel<<<(unsigned)((rows_total * 32 + 255) / 256), 256, 0, st>>>(stats, rows_total, n_kblk, row_ml);
+  dim3 g2((unsigned)((S + 255) / 256), (unsigned)n_heads);
+  vs_vertical_kernel<<<g2, 256, 0, st>>>(s, row_ml, L, S, p, vscore);
+  vs_slash_kernel<<<g2, 256, 0, st>>>(p, L, S, sscore);
+  vs_topk_kernel<<<dim3((unsigned)n_heads, 2), kTopkThreads, 0, st>>>(vscore, sscore, S, k_v, k_s, vout, sout);
+  return check_cuda(cudaGetLastError(), "vs estimate");
+}
+
+template <typename T>
+int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids, int n_heads,
+                     int k_b, int B, const int64_t* tile_offsets, int32_t* tile_starts, uint8_t* ws,
+                     cudaStream_t st) {
+  const int N = (S + B - 1) / B;
+  float* qp = reinterpret_cast<float*>(ws);
+  ws += align256((size_t)Hq * N * d * 4);
+  float* kp = reinterpret_cast<float*>(ws);
+  ws += align256((size_t)Hkv * N * d * 4);
+  double* sc = reinterpret_cast<double*>(ws);  // [n_heads][N][N]
+  int rc;
+  {
+    const int64_t tq = (int64_t)Hq * N * d, tk = (int64_t)Hkv * N * d;
+    pool_kernel<T><<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
+    pool_kernel<T><<<(unsigned)((tk + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
+    if ((rc = check_cuda(cudaGetLastError(), "bs pool"))) return rc;
+  }
+  const size_t smem = (size_t)2 * d * kLd * sizeof(double);
+  auto kern = score_tile_kernel<float, float, false>;
+  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "bs score smem attr")))
+    return rc;
+  const int nt = (N + kTile - 1) / kTile;
+  kern<<<dim3((unsigned)nt, (unsigned)nt, (unsigned)n_heads), kScoreThreads, smem, st>>>(
+      qp, kp, head_ids, Hq / Hkv, (int64_t)N * d, (int64_t)N * d, 0, N, N, d, 1.0 / sqrt((double)d), 0, sc,
+      (int64_t)N * N, nullptr, 0);
+  if ((rc = check_cuda(cudaGetLastError(), "bs score"))) return rc;
+  const size_t rsmem = (size_t)N * sizeof(float);
+  if ((rc = check_cuda(cudaFuncSetAttribute(bs_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem),
+                       "bs row smem attr")))
+    return rc;
+  bs_row_kernel<<<dim3((unsigned)N, (unsigned)n_heads), kBsThreads, rsmem, st>>>(sc, N, k_b, B, head_ids,
+                                                                                 tile_offsets, tile_starts);
+  return check_cuda(cudaGetLastError(), "bs row");
+}
+
+}  // namespace
+}  // namespace spf
+
+using namespace spf;
+
+extern "C" {
+
+size_t spf_vs_estimate_workspace_size(int n_heads, int seq_len, int last_q) {
+  const size_t L = last_q, S = seq_len, H = n_heads;
+  const size_t n_kblk = (S + kTile - 1) / kTile;
+  return align256(H * L * S * 8) + align256(H * L * S * 4) + align256(H * L * n_kblk * 16) + align256(H * L * 16) +
+         2 * align256(H * S * 8);
+}
+
+int spf_vs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+                    int head_dim, const int32_t* head_ids, int n_heads, int last_q, int k_v, int k_s,
+                    int32_t* vertical_out, int32_t* slash_out, double* vscore_out, double* sscore_out,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (last_q < 1 || k_v < 1 || k_s < 1) return set_error(SPF_ERR_INVALID, "Vertical-Slash counts must be >= 1");
+  if (last_q > seq_len) return set_error(SPF_ERR_INVALID, "last_q=%d exceeds seq_len=%d", last_q, seq_len);
+  if (head_dim < 1 || head_dim > 128) return set_error(SPF_ERR_INVALID, "head_dim must be in [1, 128]");
+  if (n_kv_heads < 1 || n_q_heads % n_kv_heads) return set_error(SPF_ERR_INVALID, "bad head counts");
+  if (n_heads <= 0) return SPF_OK;
+  const size_t need = spf_vs_estimate_workspace_size(n_heads, seq_len, last_q);
+  if (workspace == nullptr || workspace_bytes < need)
+    return set_error(SPF_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  const int kv = min(k_v, seq_len), ks = min(k_s, seq_len);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  if (dtype == SPF_DTYPE_BF16)
+    return vs_estimate_impl(reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
+                            n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks, vertical_out,
+                            slash_out, vscore_out, sscore_out, ws, st);
+  if (dtype == SPF_DTYPE_F32)
+    return vs_estimate_impl(reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k), n_q_heads,
+                            n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks, vertical_out, slash_out,
+                            vscore_out, sscore_out, ws, st);
+  return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+size_t spf_bs_estimate_workspace_size(int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int block_size) {
+  const size_t N = (seq_len + block_size - 1) / block_size;
+  return align256((size_t)n_q_heads * N * head_dim * 4) + align256((size_t)n_kv_heads * N * head_dim * 4) +
+         align256((size_t)n_q_heads * N * N * 8);
+}
+
+int spf_bs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+                    int head_dim, const int32_t* head_ids, int n_heads, int k_b, int block_size,
+                    const int64_t* tile_offsets, int32_t* tile_starts, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  if (k_b < 1 || block_size < 1) return set_error(SPF_ERR_INVALID, "Block-Sparse counts must be >= 1");
+  if (head_dim < 1 || head_dim > 128) return set_error(SPF_ERR_INVALID, "head_dim must be in [1, 128]");
+  if (n_kv_heads < 1 || n_q_heads % n_kv_heads) return set_error(SPF_ERR_INVALID, "bad head counts");
+  const int N = (seq_len + block_size - 1) / block_size;
+  if ((size_t)N * sizeof(float) > 200 * 1024)
+    return set_error(SPF_ERR_INVALID, "too many block rows (%d) for the per-row top-k", N);
+  if (n_heads <= 0) return SPF_OK;
+  // scores scratch is sized for n_heads (the heads actually estimated)
+  const size_t need = align256((size_t)n_q_heads * N * head_dim * 4) + align256((size_t)n_kv_heads * N * head_dim * 4) +
+                      align256((size_t)n_heads * N * N * 8);
+  if (workspace == nullptr || workspace_bytes < need)
+    return set_error(SPF_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  if (dtype == SPF_DTYPE_BF16)
+    return bs_estimate_impl(reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
+                            n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, k_b, block_size,
+                            tile_offsets, tile_starts, ws, st);
+  if (dtype == SPF_DTYPE_F32)
+    return bs_estimate_impl(reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k), n_q_heads,
+                            n_kv_heads, seq_len, head_dim, head_ids, n_heads, k_b, block_size, tile_offsets,
+                            tile_starts, ws, st);
+  return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+"""Production entry: one layer of dynamic sparse pre-fill attention on a B200.
+
+``sparse_prefill_attention(q, k, v, head_cfgs)`` runs, for a whole layer of
+q-heads with per-head pattern configs (patterns.py:23-57, as loaded from the
+config JSON v1 of patterns.py:236-266), the hot path of the reference's
+``run_head`` (sparse_attn.py:67-94) for every head at once:
+
+  1. online estimation      VS heads grouped by (k_v, k_s, last_q): spf_vs_estimate
+  2. index compaction       per-row counts for VS / A-shape / BS heads -> one
+                            CSR over all q-heads (spf_*_layout_count,
+                            spf_csr_offsets, spf_*_layout_fill); BS heads'
+                            pooled estimation writes its tiles directly
+  3. sparse attention       ONE launch of the sm_100a kernel over all heads
+                            and patterns (GQA head map), bf16 I/O.
+
+Everything stays on the device; the only host sync is the read-back of the
+two CSR totals needed to size the layout.
+"""
+
+from __future__ import annotations
+
+import math
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import torch
+
+from . import _dev, kernels, layouts
+from .estimator import estimate_block_sparse_gpu, estimate_vertical_slash_gpu
+from .patterns import AShape, BlockSparse, HeadPatternConfig, VerticalSlash, n_block_rows
+
+
+@dataclass
+class LayerLayout:
+    """Device CSR over (q-head, query-block row) for one layer."""
+
+    seq_len: int
+    block_size: int
+    n_heads: int
+    tiles: torch.Tensor
+    tile_offsets: torch.Tensor
+    cols: torch.Tensor
+    col_offsets: torch.Tensor
+
+    @property
+    def n_tiles(self) -> int:
+        return int(self.tiles.numel())
+
+    @property
+    def n_cols(self) -> int:
+        return int(self.cols.numel())
+
+    def chips(self) -> int:
+        """Column chips of B per row, summed (the kernel's gathered steps)."""
+        per_row = self.col_offsets[1:] - self.col_offsets[:-1]
+        return int(((per_row + self.block_size - 1) // self.block_size).sum().item())
+
+    def area(self) -> torch.Tensor:
+        """Per-head computed-cell area (patterns.py:147-184)."""
+        return layouts.layout_area_dev(self.n_heads, self.seq_len, self.block_size, self.tiles, self.tile_offsets,
+                                       self.col_offsets)
+
+    def head_rows(self, h: int):
+        n = n_block_rows(self.seq_len, self.block_size)
+        return self.tile_offsets[h * n: (h + 1) * n + 1], self.col_offsets[h * n: (h + 1) * n + 1]
+
+
+def _group_heads(head_cfgs, device):
+    groups: "OrderedDict[HeadPatternConfig, list[int]]" = OrderedDict()
+    for h, cfg in enumerate(head_cfgs):
+        if not isinstance(cfg, (AShape, VerticalSlash, BlockSparse)):
+            raise TypeError(f"unknown pattern config: {cfg!r}")
+        groups.setdefault(cfg, []).append(h)
+    return [(cfg, torch.tensor(ids, dtype=torch.int32, device=device), len(ids)) for cfg, ids in groups.items()]
+
+
+def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: int = 64,
+                       stream=None) -> LayerLayout:
+    """Estimation + index compaction for every head of a layer (steps 1-2)."""
+    dev = _dev.require_cuda(q.device)
+    hq, s_len, _ = q.shape
+    if len(head_cfgs) != hq:
+        raise ValueError(f"need one pattern config per q-head ({len(head_cfgs)} != {hq})")
+    for cfg in head_cfgs:
+        if isinstance(cfg, BlockSparse) and cfg.block_size != block_size:
+            raise ValueError("all heads of a layer must share one block size "
+                             f"(BlockSparse block_size {cfg.block_size} != {block_size})")
+    n = n_block_rows(s_len, block_size)
+    groups = _group_heads(head_cfgs, dev)
+    tc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
+    cc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
+    vs_sel = {}
+    for cfg, ids, m in groups:
+        if isinstance(cfg, VerticalSlash):
+            vert, sl = estimate_vertical_slash_gpu(q, k, cfg, ids, stream=stream)
+            vs_sel[cfg] = (vert, sl)
+            layouts.vs_count(vert, sl, ids, s_len, block_size, tc, cc, stream)
+        elif isinstance(cfg, AShape):
+            layouts.ashape_count(ids, m, s_len, block_size, cfg, tc, stream)
+        else:
+            layouts.bs_count(ids, m, s_len, block_size, cfg.k_b, tc, stream)
+    toff, _ = layouts.csr_offsets(tc, stream, want_total=False)
+    coff, _ = layouts.csr_offsets(cc, stream, want_total=False)
+    totals = torch.stack([toff[-1], coff[-1]]).cpu()  # the one host sync of the layer
+    nt, nc = int(totals[0]), int(totals[1])
+    tiles = torch.empty(max(nt, 1), dtype=torch.int32, device=dev)
+    cols = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
+    for cfg, ids, m in groups:
+        if isinstance(cfg, VerticalSlash):
+            vert, sl = vs_sel[cfg]
+            layouts.vs_fill(vert, sl, ids, s_len, block_size, toff, coff, tiles, cols, stream)
+        elif isinstance(cfg, AShape):
+            layouts.ashape_fill(ids, m, s_len, block_size, cfg, toff, tiles, stream)
+        else:
+            estimate_block_sparse_gpu(q, k, cfg, ids, toff, tiles, stream)
+    return LayerLayout(s_len, block_size, hq, tiles[:nt], toff, cols[:nc], coff)
+
+
+def sparse_prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, head_cfgs, block_size: int = 64,
+                             scale: float | None = None, out: torch.Tensor | None = None, stream=None,
+                             return_layout: bool = False):
+    """Full layer: q [Hq, S, d], k/v [Hkv, S, d] (bf16) -> out [Hq, S, d]."""
+    layout = build_layer_layout(q, k, head_cfgs, block_size, stream)
+    d = q.shape[-1]
+    sc = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    out = kernels.sparse_flash_attention_gpu(q, k, v, sc, block_size, layout.tiles, layout.tile_offsets,
+                                             layout.cols, layout.col_offsets, out=out, stream=stream)
+    return (out, layout) if return_layout else out

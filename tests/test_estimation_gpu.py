@@ -1,0 +1,122 @@
+"""Index parity of the GPU estimators against the reference (golden vectors)
+and the oracle port: index sets must be bit-exact (north_star), the fp64
+score vectors equal to ~1 ulp."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bf16_round, gaussian_qkv
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2407_02490_b200 as P
+
+    return P
+
+
+def _vs_names(golden):
+    return sorted({k.split("__")[0] for k in golden.files if k.startswith("vs_")})
+
+
+def test_vs_golden_numpy_api(golden, P):
+    for name in _vs_names(golden):
+        s, d, kv, ks, lq, seed, bf16, b = (int(x) for x in golden[f"{name}__params"])
+        q, k, _ = gaussian_qkv(s, d, seed, bool(bf16))
+        idx = P.estimate_vertical_slash(q, k, P.VerticalSlash(kv, ks, lq))
+        np.testing.assert_array_equal(idx.vertical, golden[f"{name}__vertical"], err_msg=name)
+        np.testing.assert_array_equal(idx.slash, golden[f"{name}__slash"], err_msg=name)
+
+
+def test_vs_golden_scores_and_bf16_path(golden, P):
+    for name in _vs_names(golden):
+        s, d, kv, ks, lq, seed, bf16, b = (int(x) for x in golden[f"{name}__params"])
+        if not bf16:
+            continue
+        q, k, _ = gaussian_qkv(s, d, seed, True)
+        tq = torch.from_numpy(q).cuda().to(torch.bfloat16)[None]
+        tk = torch.from_numpy(k).cuda().to(torch.bfloat16)[None]
+        vert, sl, vsc, ssc = P.estimate_vertical_slash_gpu(tq, tk, P.VerticalSlash(kv, ks, lq), with_scores=True)
+        np.testing.assert_array_equal(vert[0].cpu().numpy(), golden[f"{name}__vertical"], err_msg=name)
+        np.testing.assert_array_equal(sl[0].cpu().numpy(), golden[f"{name}__slash"], err_msg=name)
+        np.testing.assert_allclose(vsc[0].cpu().numpy(), golden[f"{name}__vscore"], rtol=1e-12, atol=0)
+        np.testing.assert_allclose(ssc[0].cpu().numpy(), golden[f"{name}__sscore"], rtol=1e-12, atol=0)
+
+
+def test_vs_gqa_multihead_matches_port(P):
+    s, d, hq, hkv = 2048, 128, 4, 2
+    rng = np.random.Generator(np.random.PCG64(7))
+    q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    cfg = P.VerticalSlash(100, 500, 64)
+    heads = torch.tensor([3, 0, 2], dtype=torch.int32, device="cuda")
+    vert, sl = P.estimate_vertical_slash_gpu(torch.from_numpy(q).cuda().to(torch.bfloat16),
+                                             torch.from_numpy(k).cuda().to(torch.bfloat16), cfg, heads)
+    for i, h in enumerate([3, 0, 2]):
+        wv, ws = port.estimate_vertical_slash(q[h], k[h // 2], 100, 500, 64)
+        np.testing.assert_array_equal(vert[i].cpu().numpy(), wv)
+        np.testing.assert_array_equal(sl[i].cpu().numpy(), ws)
+
+
+@pytest.mark.parametrize("s,d,lq", [(300, 64, 100), (1000, 128, 130), (129, 32, 129), (64, 16, 1)])
+def test_vs_last_q_variants(P, s, d, lq):
+    q, k, _ = gaussian_qkv(s, d, 100 + s)
+    idx = P.estimate_vertical_slash(q, k, P.VerticalSlash(20, 30, lq))
+    wv, ws = port.estimate_vertical_slash(q, k, 20, 30, lq)
+    np.testing.assert_array_equal(idx.vertical, wv)
+    np.testing.assert_array_equal(idx.slash, ws)
+
+
+def test_vs_rejects_last_q_over_seq_len(P):
+    q, k, _ = gaussian_qkv(8, 4, 1)
+    with pytest.raises(ValueError):
+        P.estimate_vertical_slash(q, k, P.VerticalSlash(2, 2, 16))
+
+
+def test_vs_clip_and_force_include(P):
+    q, k, _ = gaussian_qkv(8, 4, 1)
+    idx = P.estimate_vertical_slash(q, k, P.VerticalSlash(100, 100, 8))
+    assert idx.vertical.size == 8 and idx.slash.size == 8
+    q, k, _ = gaussian_qkv(64, 16, 0)
+    idx = P.estimate_vertical_slash(q, k, P.VerticalSlash(4, 4, 16))
+    assert 0 in idx.vertical and 0 in idx.slash
+
+
+def test_bs_golden(golden, P):
+    names = sorted({k.split("__")[0] for k in golden.files if k.startswith("bs_")})
+    for name in names:
+        s, d, kb, b, seed, bf16 = (int(x) for x in golden[f"{name}__params"])
+        q, k, _ = gaussian_qkv(s, d, seed, bool(bf16))
+        blocks = P.estimate_block_sparse(q, k, P.BlockSparse(kb, b))
+        flat = np.array([x * b for row in blocks.rows for x in row], dtype=np.int64)
+        np.testing.assert_array_equal(flat, golden[f"{name}__tiles"], err_msg=name)
+
+
+def test_planted_golden(golden, P):
+    q, k = golden["planted__q"], golden["planted__k"]
+    idx = P.estimate_vertical_slash(q, k, P.VerticalSlash(4, 4, 64))
+    np.testing.assert_array_equal(idx.vertical, golden["planted__vertical"])
+    np.testing.assert_array_equal(idx.slash, golden["planted__slash"])
+    assert 137 in idx.vertical and 33 in idx.slash
+    blocks = P.estimate_block_sparse(q, k, P.BlockSparse(2, 64))
+    flat = np.array([x * 64 for row in blocks.rows for x in row], dtype=np.int64)
+    np.testing.assert_array_equal(flat, golden["planted__bs_tiles"])
+
+
+@pytest.mark.parametrize("s,kb,b", [(256, 100, 64), (130, 2, 64), (777, 7, 16)])
+def test_bs_vs_port(P, s, kb, b):
+    q, k, _ = gaussian_qkv(s, 32, s + kb)
+    blocks = P.estimate_block_sparse(q, k, P.BlockSparse(kb, b))
+    assert blocks.rows == port.estimate_block_sparse(q, k, kb, b)
+
+
+def test_argtopk_ties(P):
+    np.testing.assert_array_equal(P.argtopk([1.0, 5.0, 3.0], 2), [1, 2])
+    np.testing.assert_array_equal(P.argtopk([2.0, 2.0, 2.0], 2), [0, 1])
+    assert P.argtopk([3.0, 1.0], 10).tolist() == [0, 1]
+    with pytest.raises(ValueError):
+        P.argtopk([1.0], 0)

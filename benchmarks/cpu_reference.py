@@ -1,0 +1,153 @@
+"""The reference's CPU path, timed on the host cores (bench.py's cpu_baseline
+and the ``--impl reference`` arm).  TEST/BENCH INFRASTRUCTURE: this is the
+one place bench.py executes oracle/.
+
+One work item = one (layer, head) of the benchmark config, run exactly as the
+reference's ``run_head_timed`` does (sparse_attn.py:67-94):
+  * estimation: oracle/port.py (the numpy restatement of estimator.py:82-143);
+  * index: oracle/port.py's pure-Python Alg. 4 (vs_index.py:28-95), A-shape
+    (patterns.py:109-128) or the BS tile mapping;
+  * kernel: the reference's OWN compiled Cython kernel (_core.pyx, built from
+    /root/reference into oracle/_ref by oracle/Makefile) when present, else the
+    port -- on a row sample (other rows' lists empty), extrapolated by
+    tiles + column chips (kernel time is linear in them).
+Items run in a process pool (one process per core; the Cython kernel holds the
+GIL, so threads would not help) with OPENBLAS_NUM_THREADS=1; the step's
+latency = sum(item seconds) / cores.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import numpy as np
+
+
+def g_local_np(s: int, d: int, seed: int):
+    """numpy twin of benchmarks.workloads.g_local_qkv for one head (fp32, bf16-exact)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    q = (rng.standard_normal((s, d)) * 0.5).astype(np.float32)
+    k = (rng.standard_normal((s, d)) * 0.5).astype(np.float32)
+    v = rng.standard_normal((s, d)).astype(np.float32)
+    j = np.arange(s)
+    k[:, 0] = j % 256
+    k[:, 1] = (j >> 8) % 256
+    k[:, 2] = j >> 16
+    a = 2.0 ** -3
+    q[:, 0], q[:, 1], q[:, 2] = a, a * 256, a * 65536
+    k[:4, 3] = 64.0
+    q[:, 3] = 1.0
+
+    def bf16(x):
+        u = x.view(np.uint32).astype(np.uint64)
+        u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+        return u.astype(np.uint32).view(np.float32)
+
+    return bf16(q), bf16(k), bf16(v)
+
+
+def _run_item(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    kind, params, s, d, b, seed, n_sample_rows = args
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if repo not in sys.path:
+        sys.path.insert(0, repo)
+    from oracle import port
+
+    ref = port.load_ref_core()
+    q, k, v = g_local_np(s, d, seed)
+    t0 = time.perf_counter()
+    if kind == "vertical_slash":
+        k_v, k_s, last_q = params
+        vv, ss = port.estimate_vertical_slash(q, k, k_v, k_s, last_q)
+        t1 = time.perf_counter()
+        tiles, cols, _ = port.build_vs_layout_with_stats(vv, ss, s, b)
+    elif kind == "a_shape":
+        t1 = time.perf_counter()
+        tiles = port.a_shape_layout(s, params[0], params[1], b)
+        cols = [[] for _ in tiles]
+    else:
+        rows = port.estimate_block_sparse(q, k, params[0], b)
+        t1 = time.perf_counter()
+        tiles = port.block_rows_to_tiles(rows, b)
+        cols = [[] for _ in tiles]
+    t2 = time.perf_counter()
+    n = len(tiles)
+    units = np.array([len(tiles[r]) + (len(cols[r]) + b - 1) // b for r in range(n)], dtype=np.int64)
+    sample = np.unique(np.linspace(0, n - 1, min(n_sample_rows, n)).round().astype(np.int64))
+    chosen = set(sample.tolist())
+    st = [tiles[r] if r in chosen else [] for r in range(n)]
+    sc = [cols[r] if r in chosen else [] for r in range(n)]
+    ts, to = port.flatten(st)
+    cs, co = port.flatten(sc)
+    scale = 1.0 / math.sqrt(d)
+    # fixed per-call cost (fp64 copies of q/k/v, output allocation): one call
+    # with every row empty; only the per-row work is extrapolated.
+    e_t, e_to = port.flatten([[] for _ in range(n)])
+    t3 = time.perf_counter()
+    if ref is not None:
+        ref.sparse_flash_rows(q, k, v, scale, b, e_t, e_to, e_t, e_to)
+    t4 = time.perf_counter()
+    if ref is not None:
+        ref.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co)
+    else:
+        port.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co, rows=sample)
+    t5 = time.perf_counter()
+    fixed = (t4 - t3) if ref is not None else 0.0
+    sampled_units = int(units[sample].sum())
+    total_units = int(units.sum())
+    kernel_s = fixed + max(0.0, (t5 - t4) - fixed) * total_units / max(1, sampled_units)
+    return {"kind": kind, "t_est": t1 - t0, "t_index": t2 - t1, "t_kernel": kernel_s,
+            "t_item": (t1 - t0) + (t2 - t1) + kernel_s, "units": total_units, "sampled_units": sampled_units,
+            "ref_kernel": ref is not None}
+
+
+def pattern_of(cfg):
+    name = type(cfg).__name__
+    if name == "VerticalSlash":
+        return "vertical_slash", (cfg.k_v, cfg.k_s, cfg.last_q)
+    if name == "AShape":
+        return "a_shape", (cfg.global_tokens, cfg.local_window)
+    return "block_sparse", (cfg.k_b,)
+
+
+def run_sample(layer_cfgs, s: int, d: int, b: int, cores: int, items_per_pattern: int, n_sample_rows: int,
+               step_seed: int = 0):
+    """One bounded sample: items_per_pattern (layer, head) items per pattern,
+    run on `cores` processes.  Returns (extrapolated step seconds, details)."""
+    import multiprocessing as mp
+
+    by_pattern: dict = {}
+    for layer, row in enumerate(layer_cfgs):
+        for h, cfg in enumerate(row):
+            kind, params = pattern_of(cfg)
+            by_pattern.setdefault((kind, params), []).append((layer, h))
+    rng = np.random.Generator(np.random.PCG64(1234 + step_seed))
+    jobs = []
+    for (kind, params), heads in by_pattern.items():
+        pick = rng.choice(len(heads), size=min(items_per_pattern, len(heads)), replace=False)
+        for i in pick:
+            layer, h = heads[int(i)]
+            jobs.append((kind, params, s, d, b, 1000 * layer + h, n_sample_rows))
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(processes=min(cores, len(jobs))) as pool:
+        res = pool.map(_run_item, jobs)
+    wall = time.perf_counter() - t0
+    total = 0.0
+    per = {}
+    for (kind, params), heads in by_pattern.items():
+        rs = [r for r, j in zip(res, jobs) if (j[0], j[1]) == (kind, params)]
+        mean_item = float(np.mean([r["t_item"] for r in rs]))
+        per[f"{kind}{list(params)}"] = {"heads": len(heads), "mean_item_s": mean_item,
+                                        "mean_est_s": float(np.mean([r["t_est"] for r in rs])),
+                                        "mean_index_s": float(np.mean([r["t_index"] for r in rs])),
+                                        "mean_kernel_s": float(np.mean([r["t_kernel"] for r in rs]))}
+        total += mean_item * len(heads)
+    step_s = total / cores
+    return step_s, {"items": len(jobs), "wall_s": wall, "patterns": per,
+                    "ref_kernel": all(r["ref_kernel"] for r in res)}

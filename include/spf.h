@@ -43,6 +43,9 @@ extern "C" {
 /* Library identification / error reporting. */
 int spf_version(void);
 const char* spf_last_error(void);
+/* Number of CUDA kernels this library has launched in the process (for the
+ * benchmark's gpu_launches accounting). */
+unsigned long long spf_kernel_launches(void);
 
 /* ---------------------------------------------------------------------------
  * Sparse FlashAttention forward.

@@ -26,6 +26,7 @@ _i64 = ctypes.c_int64
 SIGNATURES = {
     "spf_version": (_c_int, []),
     "spf_last_error": (ctypes.c_char_p, []),
+    "spf_kernel_launches": (ctypes.c_ulonglong, []),
     "spf_sparse_flash_workspace_size": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "spf_sparse_flash_rows": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
                                        _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),

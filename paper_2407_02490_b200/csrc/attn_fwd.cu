@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       }
       for (int sub = 0; sub * kBox < B; ++sub) {
         const int st = t % kStages;
-        mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
         if (lane == 0) {
+          mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
           StepDesc& d = ctrl->desc[st];
           d.kind = kTile;
           d.box = best + sub * kBox;
@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         for (int64_t s0 = c0; s0 < chip_end; s0 += kBox) {
           const int n = (int)min((int64_t)kBox, chip_end - s0);
           const int st = t % kStages;
-          mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
+          if (lane == 0) mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
+          __syncwarp();
           StepDesc& d = ctrl->desc[st];
           // prefix max of the keys (two 32-wide warp scans)
           int key_a = lane < n ? p.col_indices[s0 + lane] : INT_MIN;
@@ -273,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     // --- end marker ---
     {
       const int st = t % kStages;
-      mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
       if (lane == 0) {
+        mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
         ctrl->desc[st].kind = kEnd;
         mbar_arrive(&ctrl->kv_full[st]);
       }
@@ -384,15 +385,21 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
           hi = a;
         }
       }
-      const bool full = (lo == 0 && hi == kBox);
-      float mx = -INFINITY;
-      if (full) {
+      // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
+      if (!(lo == 0 && hi == kBox)) {
 #pragma unroll
-        for (int j = 0; j < kBox; ++j) mx = fmaxf(mx, u2f(x[j]));
-      } else {
-#pragma unroll
-        for (int j = 0; j < kBox; ++j) mx = (j >= lo && j < hi) ? fmaxf(mx, u2f(x[j])) : mx;
+        for (int j = 0; j < kBox; ++j) x[j] = (j >= lo && j < hi) ? x[j] : 0xff800000u;
       }
+      // row max: four independent 3-input max chains (FMNMX3)
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kBox; j += 8) {
+        mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
+        mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
+        mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
+        mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
+      }
+      const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
       float alpha = 1.f;
       bool rescale = false;
       if (hi > lo) {
@@ -407,14 +414,24 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       }
       uint32_t ph[kBox / 2];
       uint32_t pl[kSplit ? kBox / 2 : 1];
-      float sum = 0.f;
-      const float neg_m = -m_run;
+      // p = 2^(x*c - m): packed FFMA2, MUFU ex2, packed FADD2 row sums
+      const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+      const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
+      const uint64_t m2 = pack_f32x2(neg_m, neg_m);
+      uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
 #pragma unroll
       for (int j = 0; j < kBox; j += 2) {
-        float p0 = 0.f, p1 = 0.f;
-        if (full || (j >= lo && j < hi)) p0 = ex2_approx(fmaf(u2f(x[j]), scale_log2, neg_m));
-        if (full || (j + 1 >= lo && j + 1 < hi)) p1 = ex2_approx(fmaf(u2f(x[j + 1]), scale_log2, neg_m));
-        sum += p0 + p1;
+        const uint64_t y = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
+        float y0, y1;
+        unpack_f32x2(y, y0, y1);
+        const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+        const uint64_t pp = pack_f32x2(p0, p1);
+        switch ((j >> 1) & 3) {
+          case 0: s0 = fadd2(s0, pp); break;
+          case 1: s1 = fadd2(s1, pp); break;
+          case 2: s2 = fadd2(s2, pp); break;
+          default: s3 = fadd2(s3, pp); break;
+        }
         ph[j >> 1] = pack_bf16x2(p0, p1);
         if (kSplit) {
           const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&ph[j >> 1]);
@@ -422,6 +439,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
           pl[j >> 1] = pack_bf16x2(p0 - hf.x, p1 - hf.y);
         }
       }
+      float sa, sb2;
+      unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
+      const float sum = sa + sb2;
       l_run = l_run * alpha + sum;
 
       if (t > 0) {
@@ -542,6 +562,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
   if (grid == 0) return 0;
   if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
   const float scale_log2 = a.scale * 1.4426950408889634f;
+  note_launches(1);
   kern<<<(unsigned)grid, kThreads, L::kSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
   return check_cuda(cudaGetLastError(), "sparse_attn_fwd launch");
 }

@@ -12,6 +12,9 @@
 namespace spf {
 
 static thread_local char g_err[1024] = "";
+static unsigned long long g_launches = 0;
+
+void note_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -76,6 +79,7 @@ static int prep_operand(const void* src, __nv_bfloat16* hi, __nv_bfloat16* lo, i
   if (n == 0) return SPF_OK;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+  note_launches(1);
   prep_operand_kernel<Tin, kSplit><<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<const Tin*>(src), hi, lo,
                                                                          rows, d, kD);
   return check_cuda(cudaGetLastError(), "prep_operand");
@@ -97,6 +101,8 @@ extern "C" {
 int spf_version(void) { return 1; }
 
 const char* spf_last_error(void) { return spf::g_err; }
+
+unsigned long long spf_kernel_launches(void) { return __atomic_load_n(&spf::g_launches, __ATOMIC_RELAXED); }
 
 static int padded_dim(int d) { return d <= 64 ? 64 : 128; }
 
@@ -189,6 +195,7 @@ int spf_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
   if (n <= 0) return SPF_OK;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+  note_launches(1);
   f32_to_bf16_kernel<<<(unsigned)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       src, reinterpret_cast<__nv_bfloat16*>(dst), n);
   return check_cuda(cudaGetLastError(), "f32_to_bf16");

@@ -295,6 +295,7 @@ int vs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, cons
                        "score smem attr")))
     return rc;
   dim3 grid((unsigned)n_kblk, (unsigned)((L + kTile - 1) / kTile), (unsigned)n_heads);
+  note_launches(5);  // score, rowstats, vertical, slash, top-k
   kern<<<grid, kScoreThreads, smem, st>>>(q, k, head_ids, Hq / Hkv, (int64_t)S * d, (int64_t)S * d, S - L, L, S, d,
                                           1.0 / sqrt((double)d), S - L, s, (int64_t)L * S, stats, n_kblk);
   if ((rc = check_cuda(cudaGetLastError(), "vs score"))) return rc;
@@ -320,6 +321,7 @@ int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, cons
   int rc;
   {
     const int64_t tq = (int64_t)Hq * N * d, tk = (int64_t)Hkv * N * d;
+    note_launches(4);  // pool q, pool k, block scores, row top-k
     pool_kernel<T><<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
     pool_kernel<T><<<(unsigned)((tk + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
     if ((rc = check_cuda(cudaGetLastError(), "bs pool"))) return rc;

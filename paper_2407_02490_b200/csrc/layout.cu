@@ -210,6 +210,7 @@ int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t*
     cub::DeviceScan::InclusiveSum(nullptr, bytes, counts, offsets + 1, n);
     if (workspace == nullptr || workspace_bytes < bytes)
       return set_error(SPF_ERR_INVALID, "scan workspace too small (%zu < %zu)", workspace_bytes, bytes);
+    note_launches(2);
     if ((rc = check_cuda(cub::DeviceScan::InclusiveSum(workspace, bytes, counts, offsets + 1, n, st), "csr scan")))
       return rc;
   }
@@ -228,6 +229,7 @@ int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, 
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
   const size_t smem = (n_v + n_s <= kSmemIdx) ? (size_t)(n_v + n_s) * 4 : 0;
+  note_launches(1);
   vs_merge_kernel<false><<<row_grid(seq_len, block_size, n_heads), kThreads, smem,
                            reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
                                                                      block_size, tile_counts, col_counts, nullptr,
@@ -241,6 +243,7 @@ int spf_vs_layout_fill(const int32_t* vertical, int n_v, const int32_t* slash, i
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
   const size_t smem = (n_v + n_s <= kSmemIdx) ? (size_t)(n_v + n_s) * 4 : 0;
+  note_launches(1);
   vs_merge_kernel<true><<<row_grid(seq_len, block_size, n_heads), kThreads, smem,
                           reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
                                                                     block_size, nullptr, nullptr, tile_offsets,
@@ -253,6 +256,7 @@ int spf_ashape_layout_count(const int32_t* head_ids, int n_heads, int seq_len, i
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (global_tokens < 1 || local_window < 1) return set_error(SPF_ERR_INVALID, "A-shape counts must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
+  note_launches(1);
   ashape_kernel<<<row_grid(seq_len, block_size, n_heads), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       head_ids, seq_len, block_size, global_tokens, local_window, tile_counts, nullptr, nullptr);
   return check_cuda(cudaGetLastError(), "ashape_layout_count");
@@ -262,6 +266,7 @@ int spf_ashape_layout_fill(const int32_t* head_ids, int n_heads, int seq_len, in
                            int local_window, const int64_t* tile_offsets, int32_t* tile_starts, void* stream) {
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
+  note_launches(1);
   ashape_kernel<<<row_grid(seq_len, block_size, n_heads), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       head_ids, seq_len, block_size, global_tokens, local_window, nullptr, tile_offsets, tile_starts);
   return check_cuda(cudaGetLastError(), "ashape_layout_fill");
@@ -271,6 +276,7 @@ int spf_bs_layout_count(const int32_t* head_ids, int n_heads, int seq_len, int b
                         int64_t* tile_counts, void* stream) {
   if (block_size < 1 || k_b < 1) return set_error(SPF_ERR_INVALID, "Block-Sparse counts must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
+  note_launches(1);
   bs_count_kernel<<<row_grid(seq_len, block_size, n_heads), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       head_ids, seq_len, block_size, k_b, tile_counts);
   return check_cuda(cudaGetLastError(), "bs_layout_count");
@@ -285,6 +291,7 @@ int spf_layout_area(int n_heads, int seq_len, int block_size, const int32_t* til
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
   const int n_rows = (seq_len + block_size - 1) / block_size;
   const unsigned gx = (unsigned)min(64, (n_rows + 255) / 256);
+  note_launches(1);
   area_kernel<<<dim3(gx, (unsigned)n_heads), 256, 0, st>>>(seq_len, block_size, tile_starts, tile_offsets,
                                                            col_offsets, reinterpret_cast<unsigned long long*>(area_out));
   return check_cuda(cudaGetLastError(), "layout_area");

@@ -11,6 +11,9 @@ namespace spf {
 int set_error(int code, const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* what);
 
+// Counts kernel launches issued by this library (spf_kernel_launches()).
+void note_launches(int n);
+
 // Encodes a 3-D [dim2][dim1][dim0] bf16 tensor map with a (64 x rows x 1) box
 // and 128-byte swizzle; used for every Q/K/V operand.
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, int dim0, int dim1, int dim2, int box_rows);

@@ -75,20 +75,32 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
  * Vertical-Slash online estimation.
  * Replaces estimator.py:82-114 (estimate_vertical_slash): probabilities of
  * the last `last_q` query rows against all keys (scale 1/sqrt(head_dim),
- * causal), computed from fp64 scores and rounded to fp32 (tensor.py:78),
- * summed per column (vertical) and per diagonal offset (slash) in fp64 in the
- * reference's order, then top-k with ties to the lower index and index 0
- * force-included (estimator.py:59-79).
+ * causal), rounded to fp32 (tensor.py:78), summed per column (vertical) and
+ * per diagonal offset (slash), then top-k with ties to the lower index and
+ * index 0 force-included (estimator.py:59-79).
+ *   mode SPF_VS_EXACT : scores in fp64 from the bf16/fp32 inputs, sums in
+ *                       fp64 in the reference's order (any shape);
+ *   mode SPF_VS_FAST  : scores on the tensor cores (tcgen05, fp32 accumulate)
+ *                       for bf16 inputs with head_dim 64/128 and last_q 64
+ *                       (other shapes run the exact path).  The top-k of each
+ *                       head is certified against this path's error model;
+ *                       uncertain_out[i] = 1 marks a head whose selection is
+ *                       too close to call, which the caller re-runs with
+ *                       SPF_VS_EXACT to get the reference's set.
  *   vertical_out : [n_heads][min(k_v, S)] int32, ascending
  *   slash_out    : [n_heads][min(k_s, S)] int32, descending
  *   vscore_out / sscore_out : optional [n_heads][seq_len] fp64 score vectors
  *                  (may be NULL; used for parity tests)
+ *   uncertain_out: optional [n_heads] int32 (always 0 for SPF_VS_EXACT)
  * ------------------------------------------------------------------------- */
-size_t spf_vs_estimate_workspace_size(int n_heads, int seq_len, int last_q);
-int spf_vs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+#define SPF_VS_EXACT 0
+#define SPF_VS_FAST 1
+size_t spf_vs_estimate_workspace_size(int mode, int dtype, int n_q_heads, int n_kv_heads, int n_heads, int seq_len,
+                                      int head_dim, int last_q);
+int spf_vs_estimate(int mode, int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
                     int head_dim, const int32_t* head_ids, int n_heads, int last_q, int k_v, int k_s,
                     int32_t* vertical_out, int32_t* slash_out, double* vscore_out, double* sscore_out,
-                    void* workspace, size_t workspace_bytes, void* stream);
+                    int32_t* uncertain_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Block-Sparse online estimation.

@@ -15,6 +15,8 @@ LIB_PATH = os.path.join(_PKG, "libspf.so")
 
 SPF_DTYPE_BF16 = 0
 SPF_DTYPE_F32 = 1
+SPF_VS_EXACT = 0
+SPF_VS_FAST = 1
 
 _c_int = ctypes.c_int
 _c_float = ctypes.c_float
@@ -30,9 +32,9 @@ SIGNATURES = {
     "spf_sparse_flash_workspace_size": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "spf_sparse_flash_rows": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
                                        _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
-    "spf_vs_estimate_workspace_size": (_c_size, [_c_int, _c_int, _c_int]),
-    "spf_vs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
-                                 _c_int, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "spf_vs_estimate_workspace_size": (_c_size, [_c_int] * 8),
+    "spf_vs_estimate": (_c_int, [_c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
+                                 _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "spf_bs_estimate_workspace_size": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "spf_bs_estimate": (_c_int, [_c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
                                  _vp, _vp, _vp, _c_size, _vp]),

@@ -1,6 +1,8 @@
 // estimate.cu -- online sparse-index estimation on the GPU.
 //
-// Vertical-Slash, estimator.py:82-114 (rounding points of tensor.py:61-78):
+// Vertical-Slash: see estimate_vs_tc.cu (tensor cores, production) and
+// estimate_vs_exact.cu (fp64).  The description below is the reference
+// algorithm both follow, estimator.py:82-114 (rounding points of tensor.py:61-78):
 //   1. score pass   s[i][j] = scale * (q_tail[i] . k[j]) in fp64 (exact-enough:
 //                   bf16/fp32 inputs, fp64 FMA chain), masked j > abs_i, plus
 //                   per-(row, 64-key block) partial (max, sum exp);
@@ -122,88 +124,6 @@ __global__ void __launch_bounds__(kScoreThreads) score_tile_kernel(
   }
 }
 
-// One warp per (head, tail row): combine the partial stats (fixed order).
-__global__ void vs_rowstats_kernel(const double2* __restrict__ stats, int n_rows_total, int n_kblk,
-                                   double2* __restrict__ row_ml) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= n_rows_total) return;
-  const double2* st = stats + (int64_t)w * n_kblk;
-  double m = -INFINITY, l = 0.0;
-  for (int b = lane; b < n_kblk; b += 32) {
-    const double2 v = st[b];
-    if (v.x == -INFINITY) continue;
-    if (v.x > m) {
-      l = l * exp(m - v.x) + v.y;
-      m = v.x;
-    } else {
-      l += v.y * exp(v.x - m);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
-    const double l2 = __shfl_xor_sync(0xffffffffu, l, o);
-    const double mn = fmax(m, m2);
-    double ln = 0.0;
-    if (mn != -INFINITY) ln = (m == -INFINITY ? 0.0 : l * exp(m - mn)) + (m2 == -INFINITY ? 0.0 : l2 * exp(m2 - mn));
-    m = mn;
-    l = ln;
-  }
-  if (lane == 0) row_ml[w] = make_double2(m, l);
-}
-
-// p = fp32(exp(s - m)/l); vertical[j] = sum_i p (i ascending); p kept for the slash pass.
-__global__ void vs_vertical_kernel(const double* __restrict__ s, const double2* __restrict__ row_ml, int L, int S,
-                                   float* __restrict__ p, double* __restrict__ vertical) {
-  const int hi = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= S) return;
-  const double* sh = s + (int64_t)hi * L * S;
-  float* ph = p + (int64_t)hi * L * S;
-  const double2* ml = row_ml + (int64_t)hi * L;
-  double acc = 0.0;
-  for (int i = 0; i < L; ++i) {
-    const int abs_i = S - L + i;
-    float pv = 0.f;
-    if (j <= abs_i) {
-      const double2 st = ml[i];
-      pv = __double2float_rn(exp(sh[(int64_t)i * S + j] - st.x) / st.y);
-    }
-    ph[(int64_t)i * S + j] = pv;
-    acc += (double)pv;
-  }
-  vertical[(int64_t)hi * S + j] = acc;
-}
-
-__global__ void vs_slash_kernel(const float* __restrict__ p, int L, int S, double* __restrict__ slash) {
-  const int hi = blockIdx.y;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= S) return;
-  const float* ph = p + (int64_t)hi * L * S;
-  double acc = 0.0;
-  for (int i = 0; i < L; ++i) {
-    const int j = S - L + i - o;
-    if (j >= 0) acc += (double)ph[(int64_t)i * S + j];
-  }
-  slash[(int64_t)hi * S + o] = acc;
-}
-
-constexpr int kTopkThreads = 1024;
-
-__global__ void __launch_bounds__(kTopkThreads) vs_topk_kernel(const double* __restrict__ vscore,
-                                                               const double* __restrict__ sscore, int S, int k_v,
-                                                               int k_s, int32_t* __restrict__ vert_out,
-                                                               int32_t* __restrict__ slash_out) {
-  using TK = BlockTopK<kTopkThreads, double>;
-  __shared__ typename TK::Storage sm;
-  const int hi = blockIdx.x;
-  if (blockIdx.y == 0)
-    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, 0, false, vert_out + (int64_t)hi * k_v, 1);
-  else
-    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, 0, true, slash_out + (int64_t)hi * k_s, 1);
-}
-
 // ---------------------------------------------------------------- Block-Sparse
 template <typename T>
 __global__ void pool_kernel(const T* __restrict__ x, int64_t n_rows_total, int S, int d, int B,
@@ -268,47 +188,6 @@ __global__ void __launch_bounds__(kBsThreads) bs_row_kernel(const double* __rest
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 template <typename T>
-int vs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids, int n_heads,
-                     int L, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                     uint8_t* ws, cudaStream_t st) {
-  const int n_kblk = (S + kTile - 1) / kTile;
-  double* s = reinterpret_cast<double*>(ws);
-  ws += align256((size_t)n_heads * L * S * 8);
-  float* p = reinterpret_cast<float*>(ws);
-  ws += align256((size_t)n_heads * L * S * 4);
-  double2* stats = reinterpret_cast<double2*>(ws);
-  ws += align256((size_t)n_heads * L * n_kblk * 16);
-  double2* row_ml = reinterpret_cast<double2*>(ws);
-  ws += align256((size_t)n_heads * L * 16);
-  if (vscore == nullptr) {
-    vscore = reinterpret_cast<double*>(ws);
-    ws += align256((size_t)n_heads * S * 8);
-  }
-  if (sscore == nullptr) {
-    sscore = reinterpret_cast<double*>(ws);
-    ws += align256((size_t)n_heads * S * 8);
-  }
-  const size_t smem = (size_t)2 * d * kLd * sizeof(double);
-  auto kern = score_tile_kernel<T, T, true>;
-  int rc;
-  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                       "score smem attr")))
-    return rc;
-  dim3 grid((unsigned)n_kblk, (unsigned)((L + kTile - 1) / kTile), (unsigned)n_heads);
-  note_launches(5);  // score, rowstats, vertical, slash, top-k
-  kern<<<grid, kScoreThreads, smem, st>>>(q, k, head_ids, Hq / Hkv, (int64_t)S * d, (int64_t)S * d, S - L, L, S, d,
-                                          1.0 / sqrt((double)d), S - L, s, (int64_t)L * S, stats, n_kblk);
-  if ((rc = check_cuda(cudaGetLastError(), "vs score"))) return rc;
-  const int rows_total = n_heads * L;
-  vs_rowstats_kernel<<<(unsigned)((rows_total * 32 + 255) / 256), 256, 0, st>>>(stats, rows_total, n_kblk, row_ml);
-  dim3 g2((unsigned)((S + 255) / 256), (unsigned)n_heads);
-  vs_vertical_kernel<<<g2, 256, 0, st>>>(s, row_ml, L, S, p, vscore);
-  vs_slash_kernel<<<g2, 256, 0, st>>>(p, L, S, sscore);
-  vs_topk_kernel<<<dim3((unsigned)n_heads, 2), kTopkThreads, 0, st>>>(vscore, sscore, S, k_v, k_s, vout, sout);
-  return check_cuda(cudaGetLastError(), "vs estimate");
-}
-
-template <typename T>
 int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids, int n_heads,
                      int k_b, int B, const int64_t* tile_offsets, int32_t* tile_starts, uint8_t* ws,
                      cudaStream_t st) {
@@ -352,37 +231,40 @@ using namespace spf;
 
 extern "C" {
 
-size_t spf_vs_estimate_workspace_size(int n_heads, int seq_len, int last_q) {
-  const size_t L = last_q, S = seq_len, H = n_heads;
-  const size_t n_kblk = (S + kTile - 1) / kTile;
-  return align256(H * L * S * 8) + align256(H * L * S * 4) + align256(H * L * n_kblk * 16) + align256(H * L * 16) +
-         2 * align256(H * S * 8);
+size_t spf_vs_estimate_workspace_size(int mode, int dtype, int n_q_heads, int n_kv_heads, int n_heads, int seq_len,
+                                      int head_dim, int last_q) {
+  if (mode == SPF_VS_FAST && vs_fast_supported(dtype, head_dim, seq_len, last_q))
+    return vs_fast_workspace_size(n_q_heads, n_kv_heads, n_heads, seq_len);
+  return vs_exact_workspace_size(n_heads, seq_len, last_q);
 }
 
-int spf_vs_estimate(int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
+int spf_vs_estimate(int mode, int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,
                     int head_dim, const int32_t* head_ids, int n_heads, int last_q, int k_v, int k_s,
                     int32_t* vertical_out, int32_t* slash_out, double* vscore_out, double* sscore_out,
-                    void* workspace, size_t workspace_bytes, void* stream) {
+                    int32_t* uncertain_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (mode != SPF_VS_EXACT && mode != SPF_VS_FAST) return set_error(SPF_ERR_INVALID, "unknown estimation mode %d", mode);
+  if (dtype != SPF_DTYPE_BF16 && dtype != SPF_DTYPE_F32) return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
   if (last_q < 1 || k_v < 1 || k_s < 1) return set_error(SPF_ERR_INVALID, "Vertical-Slash counts must be >= 1");
   if (last_q > seq_len) return set_error(SPF_ERR_INVALID, "last_q=%d exceeds seq_len=%d", last_q, seq_len);
   if (head_dim < 1 || head_dim > 128) return set_error(SPF_ERR_INVALID, "head_dim must be in [1, 128]");
   if (n_kv_heads < 1 || n_q_heads % n_kv_heads) return set_error(SPF_ERR_INVALID, "bad head counts");
   if (n_heads <= 0) return SPF_OK;
-  const size_t need = spf_vs_estimate_workspace_size(n_heads, seq_len, last_q);
+  const size_t need = spf_vs_estimate_workspace_size(mode, dtype, n_q_heads, n_kv_heads, n_heads, seq_len, head_dim,
+                                                     last_q);
   if (workspace == nullptr || workspace_bytes < need)
     return set_error(SPF_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
   const int kv = min(k_v, seq_len), ks = min(k_s, seq_len);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  if (dtype == SPF_DTYPE_BF16)
-    return vs_estimate_impl(reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
-                            n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks, vertical_out,
-                            slash_out, vscore_out, sscore_out, ws, st);
-  if (dtype == SPF_DTYPE_F32)
-    return vs_estimate_impl(reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k), n_q_heads,
-                            n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks, vertical_out, slash_out,
-                            vscore_out, sscore_out, ws, st);
-  return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
+  if (mode == SPF_VS_FAST && vs_fast_supported(dtype, head_dim, seq_len, last_q))
+    return vs_estimate_fast(q, k, n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, kv, ks, vertical_out,
+                            slash_out, vscore_out, sscore_out, uncertain_out, ws, st);
+  if (uncertain_out != nullptr) {
+    int rc = check_cuda(cudaMemsetAsync(uncertain_out, 0, (size_t)n_heads * sizeof(int32_t), st), "memset flags");
+    if (rc) return rc;
+  }
+  return vs_exact_run(dtype, q, k, n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks,
+                      vertical_out, slash_out, vscore_out, sscore_out, nullptr, nullptr, nullptr, ws, st);
 }
 
 size_t spf_bs_estimate_workspace_size(int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int block_size) {

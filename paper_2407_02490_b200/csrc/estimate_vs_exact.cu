@@ -1,0 +1,370 @@
+// estimate_vs_exact.cu -- Vertical-Slash estimation with fp64 scores (mode
+// SPF_VS_EXACT, and the in-stream fallback of SPF_VS_FAST for the heads whose
+// tensor-core selection could not be certified).
+//
+// Follows estimator.py:82-114 with the rounding points of tensor.py:61-78:
+//   s   = scale * (q_tail[i] . k[j])            fp64 FMA chain over d
+//   m_i = max_j s, l_i = sum_j exp(s - m_i)     fp64 (deterministic order)
+//   p   = fp32(exp(s - m_i) / l_i)              the reference's fp32 rounding
+//   vertical[j] = sum_i p (i ascending, fp64)   est.sum(axis=0)
+//   slash[o]    = sum_i p[i][abs_i - o] (fp64)  np.bincount over the row-major order
+//
+// Streaming design (no [rows x S] score matrix): the key axis is cut into
+// items of KB keys (KB = 64, or the multiple of 64 >= last_q - 1 so a
+// diagonal spans at most two items).  Pass A computes per-(row, item) partial
+// (max, sum exp); a combine fixes (m_i, l_i); pass B recomputes the scores,
+// forms p, sums columns in-CTA in row order and diagonals in-CTA, and adds
+// each diagonal's (at most two) item partials with fp64 atomics into a
+// zeroed vector -- two-term sums are order-free, so the result is
+// deterministic.
+//
+// Fallback mode: `gate` restricts the work to flagged heads (device-side, no
+// host sync) and `tile_max` (per row and 128-key tile, from the tensor-core
+// pass) lets an item be skipped when every score in it is below the row max
+// by more than 152 in log2 units: such p are < 2^-150 and round to exactly 0
+// in fp32 (l_i >= 1), i.e. the skip is exact, not an approximation.
+#include <cuda_bf16.h>
+
+#include "spf.h"
+#include "spf_internal.h"
+#include "cluster_topk.cuh"
+
+namespace spf {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRowT = 64;    // rows per register tile
+constexpr int kKeyT = 64;    // keys per register tile
+constexpr int kDc = 32;      // d chunk staged in shared memory
+constexpr int kLd = 68;      // padded leading dimension (doubles) of the staged chunks
+constexpr int kMaxL = 2048;  // last_q supported by this path
+
+struct ExArgs {
+  int S, d, L, KB, n_kblk, n_heads, hpk;
+  const int32_t* head_ids;
+  const int32_t* gate;     // nullable
+  const float* tile_max;   // nullable: [n_heads][64][ceil(S/128)] raw fp32 scores
+  const float* row_mc;     // [n_heads][64]: fp32(max raw score * c)
+  float c;                 // scale * log2(e)
+  double scale;
+  double2* stats;          // [n_heads][L][n_kblk]
+  double2* row_ml;         // [n_heads][L]
+  double* vscore;          // [n_heads][S]
+  double* sscore;          // [n_heads][S]
+};
+
+template <typename T>
+__device__ __forceinline__ double ld_f64(const T* p) {
+  return static_cast<double>(static_cast<float>(*p));
+}
+template <>
+__device__ __forceinline__ double ld_f64<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return static_cast<double>(__bfloat162float(*p));
+}
+
+struct ExSmem {
+  double At[kDc * kLd];
+  double Bt[kDc * kLd];
+  float P[kRowT][kKeyT + 1];
+};
+
+// acc[4][4] = q_tail rows (r0 + 4 tr + a) . keys (k0 + 4 tk + b), fp64, d ascending
+template <typename T>
+__device__ void score_tile(ExSmem& sm, const T* qh, const T* kh, int r0, int n_rows_valid, int k0, int S, int d,
+                           double (&acc)[4][4]) {
+  const int tid = threadIdx.x, tr = tid >> 4, tk = tid & 15;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int c0 = 0; c0 < d; c0 += kDc) {
+    __syncthreads();
+    for (int e = tid; e < kRowT * kDc; e += kThreads) {
+      const int r = e / kDc, c = e % kDc;
+      const bool okc = c0 + c < d;
+      sm.At[c * kLd + r] = (okc && r < n_rows_valid) ? ld_f64(qh + (int64_t)(r0 + r) * d + c0 + c) : 0.0;
+      sm.Bt[c * kLd + r] = (okc && k0 + r < S) ? ld_f64(kh + (int64_t)(k0 + r) * d + c0 + c) : 0.0;
+    }
+    __syncthreads();
+    const int cn = min(kDc, d - c0);
+    for (int c = 0; c < cn; ++c) {
+      const double2 qa = *reinterpret_cast<const double2*>(sm.At + c * kLd + 4 * tr);
+      const double2 qb = *reinterpret_cast<const double2*>(sm.At + c * kLd + 4 * tr + 2);
+      const double2 ka = *reinterpret_cast<const double2*>(sm.Bt + c * kLd + 4 * tk);
+      const double2 kb = *reinterpret_cast<const double2*>(sm.Bt + c * kLd + 4 * tk + 2);
+      const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
+      const double kv[4] = {ka.x, ka.y, kb.x, kb.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(qv[a], kv[b], acc[a][b]);
+    }
+  }
+}
+
+// Is any score of item (h, kb) within 152 (log2 units) of its row max?  Exact-skip test.
+__device__ bool item_significant(const ExArgs& a, int h, int k0) {
+  if (a.tile_max == nullptr) return true;
+  const int n_t = (a.S + 127) / 128;
+  const int t = k0 / 128;
+  int sig = 0;
+  if (threadIdx.x < 64) {
+    const float tm = a.tile_max[((int64_t)h * 64 + threadIdx.x) * n_t + t];
+    const float mc = a.row_mc[(int64_t)h * 64 + threadIdx.x];
+    sig = !(tm * a.c - mc < -152.f);  // NaN-safe: anything unexpected counts as significant
+  }
+  return __syncthreads_or(sig) != 0;
+}
+
+template <typename T, int kPass>
+__global__ void __launch_bounds__(kThreads) vs_exact_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                            const ExArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  ExSmem& sm = *reinterpret_cast<ExSmem*>(smraw);
+  double* colsum = reinterpret_cast<double*>(smraw + sizeof(ExSmem));   // [KB]
+  double* diagsum = colsum + a.KB;                                      // [KB + L - 1]
+  const int tid = threadIdx.x, tr = tid >> 4, tk = tid & 15;
+  const int S = a.S, L = a.L, KB = a.KB, d = a.d;
+  const int n_rt = (L + kRowT - 1) / kRowT;
+  // items (head, key block) interleaved head-fastest, so the significant blocks of every
+  // flagged head (often a narrow band of keys) spread over all CTAs
+  const int64_t n_items = (int64_t)a.n_heads * a.n_kblk;
+  for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int h = (int)(w % a.n_heads);
+    const int kb = (int)(w / a.n_heads);
+    if (a.gate != nullptr && a.gate[h] == 0) continue;
+    const int qh_id = a.head_ids ? a.head_ids[h] : h;
+    const T* qh = q + ((int64_t)qh_id * S + (S - L)) * d;
+    const T* kh = k + (int64_t)(qh_id / a.hpk) * S * d;
+    {
+      const int k0 = kb * KB;
+      if (kPass == 1) {  // zero this item's share of the slash vector (pass 2 accumulates into it)
+        for (int o = k0 + tid; o < min(k0 + KB, S); o += kThreads) a.sscore[(int64_t)h * S + o] = 0.0;
+      }
+      const bool sig = item_significant(a, h, k0);
+      if (!sig) {
+        if (kPass == 1) {
+          for (int i = tid; i < L; i += kThreads)
+            a.stats[((int64_t)h * L + i) * a.n_kblk + kb] = make_double2(-INFINITY, 0.0);
+        } else {
+          for (int j = k0 + tid; j < min(k0 + KB, S); j += kThreads) a.vscore[(int64_t)h * S + j] = 0.0;
+        }
+        continue;
+      }
+      if (kPass == 2) {
+        for (int x = tid; x < KB + L - 1; x += kThreads) diagsum[x] = 0.0;
+        for (int x = tid; x < KB; x += kThreads) colsum[x] = 0.0;
+      }
+      for (int rt = 0; rt < n_rt; ++rt) {
+        const int r0 = rt * kRowT;
+        const int nrv = min(kRowT, L - r0);
+        double m_run[4], l_run[4];
+        double mrow[4], ilrow[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          m_run[x] = -INFINITY;
+          l_run[x] = 0.0;
+          const int i = r0 + 4 * tr + x;
+          if (kPass == 2 && i < L) {
+            const double2 ml = a.row_ml[(int64_t)h * L + i];
+            mrow[x] = ml.x;
+            ilrow[x] = ml.y;
+          } else {
+            mrow[x] = 0.0;
+            ilrow[x] = 0.0;
+          }
+        }
+        for (int sb = 0; sb < KB / kKeyT; ++sb) {
+          const int kk0 = k0 + sb * kKeyT;
+          double acc[4][4];
+          score_tile(sm, qh, kh, r0, nrv, kk0, S, d, acc);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int i = r0 + 4 * tr + x;
+            const int abs_i = S - L + i;
+            double s[4];
+            double mx = -INFINITY;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              const int j = kk0 + 4 * tk + y;
+              const bool valid = i < L && j <= abs_i;  // abs_i < S
+              s[y] = valid ? a.scale * acc[x][y] : -INFINITY;
+              mx = fmax(mx, s[y]);
+            }
+            if (kPass == 1) {
+#pragma unroll
+              for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              double l = 0.0;
+              if (mx != -INFINITY) {
+#pragma unroll
+                for (int y = 0; y < 4; ++y)
+                  if (s[y] != -INFINITY) l += exp(s[y] - mx);
+              }
+#pragma unroll
+              for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+              if (mx != -INFINITY) {
+                if (mx > m_run[x]) {
+                  l_run[x] = (m_run[x] == -INFINITY ? 0.0 : l_run[x] * exp(m_run[x] - mx)) + l;
+                  m_run[x] = mx;
+                } else {
+                  l_run[x] += l * exp(mx - m_run[x]);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                const float p = (s[y] == -INFINITY) ? 0.f : __double2float_rn(exp(s[y] - mrow[x]) / ilrow[x]);
+                sm.P[4 * tr + x][4 * tk + y] = p;
+              }
+            }
+          }
+          if (kPass == 2) {
+            __syncthreads();
+            // columns: rows ascending (est.sum(axis=0) order)
+            if (tid < kKeyT) {
+              double cs = colsum[sb * kKeyT + tid];
+              for (int ii = 0; ii < nrv; ++ii) cs += (double)sm.P[ii][tid];
+              colsum[sb * kKeyT + tid] = cs;
+            }
+            // diagonals of this (row tile, key tile): local key jj - row ii = cl in [-63, 63]
+            for (int cl = tid - 63; cl <= 63; cl += kThreads) {
+              const int ii0 = max(0, -cl), ii1 = min(nrv, kKeyT - cl);
+              if (ii0 >= ii1) continue;
+              const int x = sb * kKeyT - r0 + cl + (L - 1);  // diagsum index of (key - k0) - row
+              double ds = diagsum[x];
+              for (int ii = ii0; ii < ii1; ++ii) ds += (double)sm.P[ii][ii + cl];
+              diagsum[x] = ds;
+            }
+            __syncthreads();
+          }
+        }
+        if (kPass == 1 && tk == 0) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int i = r0 + 4 * tr + x;
+            if (i < L) a.stats[((int64_t)h * L + i) * a.n_kblk + kb] = make_double2(m_run[x], l_run[x]);
+          }
+        }
+      }
+      if (kPass == 2) {
+        __syncthreads();
+        for (int x = tid; x < KB; x += kThreads)
+          if (k0 + x < S) a.vscore[(int64_t)h * S + k0 + x] = colsum[x];
+        // diagonal (key - k0) - row = x - (L - 1); offset o = (S - L + row) - key
+        for (int x = tid; x < KB + L - 1; x += kThreads) {
+          const int o = S - L - k0 - (x - (L - 1));
+          if (o >= 0 && o < S && diagsum[x] != 0.0) atomicAdd(a.sscore + (int64_t)h * S + o, diagsum[x]);
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// (m_i, l_i) from the item partials: one warp per (head, row), lane-strided then a
+// fixed butterfly, so the order is deterministic.
+__global__ void vs_exact_combine_kernel(const ExArgs a) {
+  const int h = blockIdx.y;
+  if (a.gate != nullptr && a.gate[h] == 0) return;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= a.L) return;
+  const double2* st = a.stats + ((int64_t)h * a.L + i) * a.n_kblk;
+  double m = -INFINITY;
+  for (int b = lane; b < a.n_kblk; b += 32) m = fmax(m, st[b].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  double l = 0.0;
+  for (int b = lane; b < a.n_kblk; b += 32) {
+    const double2 v = st[b];
+    if (v.x != -INFINITY) l += v.y * exp(v.x - m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) a.row_ml[(int64_t)h * a.L + i] = make_double2(m, l);  // pass 2 divides by l
+}
+
+constexpr int kTopkThreads = 256;
+constexpr int kTopkCl = 8;
+
+__global__ void __cluster_dims__(kTopkCl, 1, 1) __launch_bounds__(kTopkThreads)
+    vs_exact_topk_kernel(const double* __restrict__ vscore, const double* __restrict__ sscore, int S, int k_v,
+                         int k_s, const int32_t* gate, int32_t* __restrict__ vert_out,
+                         int32_t* __restrict__ slash_out) {
+  using TK = ClusterTopK<kTopkThreads, kTopkCl>;
+  __shared__ typename TK::Storage sm;
+  const int hi = blockIdx.y;
+  if (gate != nullptr && gate[hi] == 0) return;  // cluster-uniform
+  if (blockIdx.z == 0)
+    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, false, vert_out + (int64_t)hi * k_v, nullptr, nullptr);
+  else
+    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, true, slash_out + (int64_t)hi * k_s, nullptr, nullptr);
+}
+
+int kb_for(int L) { return kKeyT * max(1, (L - 1 + kKeyT - 1) / kKeyT); }
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q) {
+  const int KB = kb_for(last_q);
+  const size_t n_kblk = (seq_len + KB - 1) / KB;
+  return al256((size_t)n_heads * last_q * n_kblk * 16) + al256((size_t)n_heads * last_q * 16) +
+         2 * al256((size_t)n_heads * seq_len * 8);
+}
+
+int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
+                 int n_heads, int L, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
+                 const int32_t* gate, const float* tile_max, const float* row_mc, void* workspace, cudaStream_t st) {
+  if (L > kMaxL) return set_error(SPF_ERR_INVALID, "last_q=%d exceeds the supported %d", L, kMaxL);
+  ExArgs a{};
+  a.S = S;
+  a.d = d;
+  a.L = L;
+  a.KB = kb_for(L);
+  a.n_kblk = (S + a.KB - 1) / a.KB;
+  a.n_heads = n_heads;
+  a.hpk = Hq / Hkv;
+  a.head_ids = head_ids;
+  a.gate = gate;
+  a.tile_max = (L == 64 && a.KB == 64) ? tile_max : nullptr;
+  a.row_mc = row_mc;
+  a.scale = 1.0 / sqrt((double)d);
+  a.c = (float)(a.scale * 1.4426950408889634);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  auto take = [&](size_t bytes) {
+    uint8_t* p = ws;
+    ws += al256(bytes);
+    return p;
+  };
+  a.stats = reinterpret_cast<double2*>(take((size_t)n_heads * L * a.n_kblk * 16));
+  a.row_ml = reinterpret_cast<double2*>(take((size_t)n_heads * L * 16));
+  a.vscore = vscore ? vscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
+  a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
+  const size_t smem = sizeof(ExSmem) + (size_t)(2 * a.KB + L - 1) * 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)a.n_kblk * n_heads, 148 * 4));
+  int rc;
+  auto launch = [&](auto k1, auto k2, const auto* qq, const auto* kk) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                         "vs exact smem")))
+      return rc;
+    if ((rc = check_cuda(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                         "vs exact smem")))
+      return rc;
+    note_launches(4);  // pass A, combine, pass B, top-k
+    k1<<<grid, kThreads, smem, st>>>(qq, kk, a);
+    vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
+    k2<<<grid, kThreads, smem, st>>>(qq, kk, a);
+    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
+                                                                                      k_s, gate, vout, sout);
+    return check_cuda(cudaGetLastError(), "vs exact");
+  };
+  if (dtype == SPF_DTYPE_BF16)
+    return launch(vs_exact_kernel<__nv_bfloat16, 1>, vs_exact_kernel<__nv_bfloat16, 2>,
+                  reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k));
+  return launch(vs_exact_kernel<float, 1>, vs_exact_kernel<float, 2>, reinterpret_cast<const float*>(q),
+                reinterpret_cast<const float*>(k));
+}
+
+}  // namespace spf

@@ -1,0 +1,577 @@
+// estimate_vs_tc.cu -- Vertical-Slash online estimation on the tensor cores
+// (the production path of spf_vs_estimate, mode SPF_VS_FAST).
+//
+// Computes the same quantities as estimator.py:82-114 -- probabilities of the
+// last 64 query rows against every key (scale 1/sqrt(d), causal), rounded to
+// fp32, summed per key column (vertical) and per diagonal offset (slash) --
+// but with the q.k scores on tcgen05 (bf16 operands, fp32 accumulate in TMEM)
+// instead of fp64.  The index sets are then certified per head (see
+// vs_topk_certify_kernel): if the k-th / (k+1)-th boundary of either top-k is
+// closer than the error model of this path, the head is flagged and the
+// caller recomputes it on the fp64 path (estimate.cu), so the selected sets
+// are those of the reference either way.
+//
+// Work decomposition:
+//   * group  = one kv head and up to 4 of its q-heads being estimated (GQA
+//              fusion: the 4 x 64 tail rows share every K tile read);
+//   * tile   = 128 consecutive keys (one TMA box per 64-wide d atom);
+//   * CTA    = (group, contiguous chunk of tiles); one CTA per SM.
+//   Pass 1 (rows in TMEM lanes): S = Qtail K^T, M=128 (two heads) x N=128 keys,
+//          per-row online (max, sum exp) -> per-chunk partial row stats.
+//   combine: per-row max / sum over chunks (fp64), inverse sums, per-head
+//          error scale.
+//   Pass 2 (keys in TMEM lanes): S^T = K Qtail^T, M=128 keys x N=64*heads,
+//          p = 2^((s-m)*c) / l per element; vertical[j] = in-thread sum over
+//          the 64 rows; slash: warp-shuffle diagonal sums, combined across
+//          warps in smem and across tiles by (exactly two-term, hence
+//          order-free) fp64 atomics into a zeroed vector.
+// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner,
+// warps 2..9 = epilogue (two warps per TMEM lane quarter).
+#include <cuda_bf16.h>
+
+#include "spf.h"
+#include "spf_internal.h"
+#include "spf_ptx.cuh"
+#include "cluster_topk.cuh"
+
+namespace spf {
+namespace {
+
+constexpr int kTailRows = 64;     // last_q supported by this path
+constexpr int kMaxMembers = 4;    // q-heads per group
+constexpr int kKeys = 128;        // keys per tile (UMMA M of pass 2, N of pass 1)
+constexpr int kStages = 4;        // K tile stages
+constexpr int kThreads = 320;     // 10 warps
+constexpr int kEpiThreads = 256;  // warps 2..9
+constexpr int kGroupRows = kMaxMembers * kTailRows;
+
+struct TcArgs {
+  int S, Hq, Hkv, hpk, gpk, n_heads, n_tiles, n_chunks;
+  const int32_t* head_ids;
+  float c_hi, c_lo;  // scale * log2(e) as an unevaluated float pair
+  // pass 1 out / combine in
+  float* st_m;       // [groups][chunks][256]  mc = fp32(row max * c)
+  double* st_l;      // [groups][chunks][256]
+  float* st_amax;    // [groups][chunks][256]
+  // combine out / pass 2 in
+  float* row_m;      // [groups][256]  mc of the global row max
+  float* row_il;     // [groups][256]
+  // pass 2 out
+  double* vscore;    // [n_heads][S]
+  double* sscore;    // [n_heads][S]  (zeroed before pass 2)
+  float* tau;        // [n_heads] relative certification threshold
+  // for the exact fallback's tile skipping
+  float* tile_max;   // [n_heads][64][n_tiles] raw row max per 128-key tile
+  float* row_mc;     // [n_heads][64] mc per slot
+};
+
+struct TcCtrl {
+  uint64_t q_full;
+  uint64_t k_full[kStages];
+  uint64_t k_empty[kStages];
+  uint64_t acc_full[2];
+  uint64_t acc_empty[2];
+  uint32_t tmem_base;
+  int nh;
+  int slot[kMaxMembers];
+  int head[kMaxMembers];
+};
+
+template <int kD>
+struct TcLayout {
+  static constexpr int kAtoms = kD / 64;
+  static constexpr int kQAtom = kGroupRows * 128;  // bytes per 64-wide d atom of the tail rows
+  static constexpr int kKAtom = kKeys * 128;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kAtoms * kQAtom;
+  static constexpr int kStageBytes = kAtoms * kKAtom;
+  static constexpr int kOffRow = kOffK + kStages * kStageBytes;      // pass 2: float2 (m, il) [256]
+  static constexpr int kOffDiag = kOffRow + kGroupRows * 8;          // pass 2: float [2][4 members][4 wk][3][32]
+  static constexpr int kDiagBytes = 2 * kMaxMembers * 4 * 3 * 32 * 4;
+  static constexpr int kOffCtrl = kOffDiag + kDiagBytes;
+  static constexpr int kSmem = kOffCtrl + (int)sizeof(TcCtrl);
+};
+
+__device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+
+// Members of group gy: the (4*sub .. 4*sub+3)-th slots (ascending) whose head maps to kv head gy / gpk.
+__device__ int group_members(const TcArgs& a, int gy, int* slot, int* head) {
+  const int kvh = gy / a.gpk, sub = gy % a.gpk;
+  int seen = 0, nh = 0;
+  for (int i = 0; i < a.n_heads; ++i) {
+    const int h = a.head_ids ? a.head_ids[i] : i;
+    if (h / a.hpk != kvh) continue;
+    if (seen >= kMaxMembers * sub && seen < kMaxMembers * (sub + 1)) {
+      slot[nh] = i;
+      head[nh] = h;
+      ++nh;
+    }
+    ++seen;
+  }
+  return nh;
+}
+
+template <int kD, int kPass>
+__global__ void __launch_bounds__(kThreads, 1)
+    vs_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, const TcArgs a) {
+  using L = TcLayout<kD>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  TcCtrl* ctrl = reinterpret_cast<TcCtrl*>(smem + L::kOffCtrl);
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gy = blockIdx.y, chunk = blockIdx.x;
+  const int S = a.S;
+  const int t_begin = (int)((int64_t)chunk * a.n_tiles / a.n_chunks);
+  const int t_end = (int)((int64_t)(chunk + 1) * a.n_tiles / a.n_chunks);
+  const int kvh = gy / a.gpk;
+
+  if (threadIdx.x == 0) {
+    ctrl->nh = group_members(a, gy, ctrl->slot, ctrl->head);
+    if ((sbase & 1023u) != 0) {
+      printf("spf: dynamic smem not 1024-aligned\n");
+      __trap();
+    }
+    mbar_init(&ctrl->q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&ctrl->k_full[s], 1);
+      mbar_init(&ctrl->k_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctrl->acc_full[b], 1);
+      mbar_init(&ctrl->acc_empty[b], kEpiThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nh = ctrl->nh;
+  if (nh == 0 || t_begin >= t_end) return;  // CTA-uniform, before TMEM allocation
+  if (kPass == 2) {
+    // row stats per member pair and tail row: {-mc(2p), -mc(2p+1), 1/l(2p), 1/l(2p+1)}
+    float4* rs = reinterpret_cast<float4*>(smem + L::kOffRow);
+    for (int r = threadIdx.x; r < 2 * kTailRows; r += kThreads) {
+      const int pr = r / kTailRows, i = r % kTailRows;
+      const int64_t b0 = (int64_t)gy * kGroupRows + (2 * pr) * kTailRows + i, b1 = b0 + kTailRows;
+      rs[r] = make_float4(-a.row_m[b0], -a.row_m[b1], a.row_il[b0], a.row_il[b1]);
+    }
+  }
+  if (warp == 1) tmem_alloc(&ctrl->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctrl->tmem_base;
+  const int n_tiles_cta = t_end - t_begin;
+
+  if (warp == 0) {
+    // =============================== TMA producer ===============================
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      mbar_arrive_expect_tx(&ctrl->q_full, (uint32_t)(nh * L::kAtoms * kTailRows * 128));
+      for (int mm = 0; mm < nh; ++mm)
+        for (int at = 0; at < L::kAtoms; ++at)
+          tma_load_3d(smem + L::kOffQ + at * L::kQAtom + mm * (kTailRows * 128), &tm_q, &ctrl->q_full, at * 64,
+                      S - kTailRows, ctrl->head[mm]);
+      for (int t = 0; t < n_tiles_cta; ++t) {
+        const int st = t % kStages;
+        mbar_wait(&ctrl->k_empty[st], ((t / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&ctrl->k_full[st], (uint32_t)L::kStageBytes);
+        uint8_t* kst = smem + L::kOffK + st * L::kStageBytes;
+        for (int at = 0; at < L::kAtoms; ++at)
+          tma_load_3d(kst + at * L::kKAtom, &tm_k, &ctrl->k_full[st], at * 64, (t_begin + t) * kKeys, kvh);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // =============================== MMA issuer =================================
+    if (lane == 0) {
+      const uint32_t q_addr = sbase + L::kOffQ;
+      mbar_wait(&ctrl->q_full, 0);
+      tc_fence_after();
+      const int nb = (nh + 1) / 2;
+      for (int t = 0; t < n_tiles_cta; ++t) {
+        const int st = t % kStages, buf = t & 1;
+        mbar_wait(&ctrl->k_full[st], (t / kStages) & 1);
+        mbar_wait(&ctrl->acc_empty[buf], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = sbase + L::kOffK + st * L::kStageBytes;
+        if (kPass == 1) {
+          constexpr uint32_t idesc = umma_idesc_bf16(128, kKeys, 0, 0);
+          for (int b = 0; b < nb; ++b) {
+#pragma unroll
+            for (int ks = 0; ks < kD / 16; ++ks) {
+              const int at = ks >> 2;
+              const uint32_t koff = (ks & 3) * 32;
+              const uint64_t ad = umma_desc_sw128(q_addr + at * L::kQAtom + b * (128 * 128) + koff, 0, 1024);
+              const uint64_t bd = umma_desc_sw128(k_addr + at * L::kKAtom + koff, 0, 1024);
+              mma_bf16_ss(tmem + buf * 256 + b * 128, ad, bd, idesc, ks > 0 ? 1u : 0u);
+            }
+          }
+        } else {
+          const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)(nh * kTailRows), 0, 0);
+#pragma unroll
+          for (int ks = 0; ks < kD / 16; ++ks) {
+            const int at = ks >> 2;
+            const uint32_t koff = (ks & 3) * 32;
+            const uint64_t ad = umma_desc_sw128(k_addr + at * L::kKAtom + koff, 0, 1024);
+            const uint64_t bd = umma_desc_sw128(q_addr + at * L::kQAtom + koff, 0, 1024);
+            mma_bf16_ss(tmem + buf * 256, ad, bd, idesc, ks > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit(&ctrl->k_empty[st]);
+        mma_commit(&ctrl->acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue warps =============================
+    // Exponents are formed as y = s*c - mc with one FFMA, c = scale*log2(e) and
+    // mc = fp32(m*c) for the running row max m.  Pass 2 reuses the very mc the
+    // row sum was taken against, so the rounding of mc cancels between p's
+    // numerator and l; packed f32x2 ops handle two values per instruction.
+    const int e = warp - 2;
+    const int quarter = warp & 3;        // TMEM lane quarter this warp may access
+    const int half = e >> 2;             // which pair of members
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float c = a.c_hi;
+    const uint64_t c2 = pack_f32x2(c, c);
+    if (kPass == 1) {
+      const int row = quarter * 32 + lane;          // row of M-block `half`
+      const int mm = 2 * half + (row >> 6);         // member (warp-uniform)
+      const int i = row & 63;
+      const int abs_i = S - kTailRows + i;
+      const bool active = mm < nh;
+      float m_run = -INFINITY, mc_run = -INFINITY, amax = 0.f;
+      double l_run = 0.0;
+      for (int t = 0; t < n_tiles_cta; ++t) {
+        const int buf = t & 1;
+        const int tile0 = (t_begin + t) * kKeys;
+        mbar_wait(&ctrl->acc_full[buf], (t >> 1) & 1);
+        tc_fence_after();
+        if (active) {
+          uint32_t x[kKeys];
+          tmem_ld32x32b_x64(tmem + lane_off + buf * 256 + half * 128, x);
+          tmem_ld32x32b_x64(tmem + lane_off + buf * 256 + half * 128 + 64, x + 64);
+          tmem_wait_ld();
+          tc_fence_before();
+          if (lane == 0) mbar_arrive(&ctrl->acc_empty[buf]);
+          const int n_valid = min(kKeys, abs_i - tile0 + 1);  // keys tile0 .. abs_i (abs_i < S)
+          float tmax = -INFINITY, tmin = INFINITY;
+          if (n_valid >= kKeys) {
+            float mx0 = -INFINITY, mx1 = -INFINITY, mn0 = INFINITY, mn1 = INFINITY;
+#pragma unroll
+            for (int j = 0; j < kKeys; j += 4) {
+              mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
+              mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
+              mn0 = fmin3(mn0, u2f(x[j]), u2f(x[j + 1]));
+              mn1 = fmin3(mn1, u2f(x[j + 2]), u2f(x[j + 3]));
+            }
+            tmax = fmaxf(mx0, mx1);
+            tmin = fminf(mn0, mn1);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kKeys; ++j) {
+              const bool ok = j < n_valid;
+              tmax = ok ? fmaxf(tmax, u2f(x[j])) : tmax;
+              tmin = ok ? fminf(tmin, u2f(x[j])) : tmin;
+              x[j] = ok ? x[j] : 0xf149f2cau;  // -1e30 (finite): 2^(y) underflows to 0
+            }
+          }
+          a.tile_max[((int64_t)ctrl->slot[mm] * kTailRows + i) * a.n_tiles + t_begin + t] = tmax;
+          if (n_valid > 0) {
+            amax = fmax3(amax, fabsf(tmax), fabsf(tmin));
+            if (tmax > m_run) {
+              const float mc_new = tmax * c;
+              if (m_run != -INFINITY) l_run *= exp2((double)mc_run - (double)mc_new);
+              m_run = tmax;
+              mc_run = mc_new;
+            }
+            const uint64_t nm2 = pack_f32x2(-mc_run, -mc_run);
+            uint64_t s0 = 0, s1 = 0;
+#pragma unroll
+            for (int j = 0; j < kKeys; j += 4) {
+              float y0, y1, y2, y3;
+              unpack_f32x2(ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, nm2), y0, y1);
+              unpack_f32x2(ffma2(pack_f32x2(u2f(x[j + 2]), u2f(x[j + 3])), c2, nm2), y2, y3);
+              s0 = fadd2(s0, pack_f32x2(ex2_approx(y0), ex2_approx(y1)));
+              s1 = fadd2(s1, pack_f32x2(ex2_approx(y2), ex2_approx(y3)));
+            }
+            float a0, a1;
+            unpack_f32x2(fadd2(s0, s1), a0, a1);
+            l_run += (double)(a0 + a1);
+          }
+        } else {
+          tc_fence_before();
+          if (lane == 0) mbar_arrive(&ctrl->acc_empty[buf]);
+        }
+      }
+      if (active) {
+        const int64_t o = ((int64_t)gy * a.n_chunks + chunk) * kGroupRows + mm * kTailRows + i;
+        a.st_m[o] = mc_run;
+        a.st_l[o] = l_run;
+        a.st_amax[o] = amax;
+      }
+    } else {
+      // row stats of this warp's member pair: {-mc(2h), -mc(2h+1), 1/l(2h), 1/l(2h+1)} per tail row
+      const float4* rs = reinterpret_cast<const float4*>(smem + L::kOffRow) + half * kTailRows;
+      float* diag = reinterpret_cast<float*>(smem + L::kOffDiag);
+      const int m0 = 2 * half, m1 = 2 * half + 1;
+      const bool act = m0 < nh;  // warp-uniform
+      const uint32_t col0 = (uint32_t)(m0 * kTailRows);
+      const uint32_t col1 = (uint32_t)((m1 < nh ? m1 : m0) * kTailRows);
+      for (int t = 0; t < n_tiles_cta; ++t) {
+        const int buf = t & 1;
+        const int tile0 = (t_begin + t) * kKeys;
+        const int j = tile0 + quarter * 32 + lane;  // this thread's key
+        mbar_wait(&ctrl->acc_full[buf], (t >> 1) & 1);
+        tc_fence_after();
+        // partial diagonal sums: [pair][wk][95][2 members]
+        float2* dbuf = reinterpret_cast<float2*>(diag + (t & 1) * (2 * 4 * 96 * 2)) + (half * 4 + quarter) * 96;
+        if (act) {
+          // row i sees key j iff j <= S - 64 + i; only the last tiles have masked rows
+          const int i_min = j - (S - kTailRows);
+          const bool full = tile0 + kKeys - 1 <= S - kTailRows;  // CTA-uniform
+          uint64_t vs0 = 0, vs1 = 0, acc = 0;
+#pragma unroll
+          for (int seg = 0; seg < 2; ++seg) {  // two 32-row halves keep the x registers at 64
+            uint32_t x0[32], x1[32];
+            tmem_ld32x32b_x32(tmem + lane_off + buf * 256 + col0 + seg * 32, x0);
+            tmem_ld32x32b_x32(tmem + lane_off + buf * 256 + col1 + seg * 32, x1);
+            tmem_wait_ld();
+            if (seg == 1) {
+              tc_fence_before();
+              if (lane == 0) mbar_arrive(&ctrl->acc_empty[buf]);
+            }
+#pragma unroll
+            for (int ii = 0; ii < 32; ++ii) {
+              const int i = seg * 32 + ii;
+              const float4 r = rs[i];
+              float y0, y1;
+              unpack_f32x2(ffma2(pack_f32x2(u2f(x0[ii]), u2f(x1[ii])), c2, pack_f32x2(r.x, r.y)), y0, y1);
+              uint64_t pp = fmul2(pack_f32x2(ex2_approx(y0), ex2_approx(y1)), pack_f32x2(r.z, r.w));
+              if (!full) pp = (i >= i_min) ? pp : 0ull;
+              if (i & 1) vs1 = fadd2(vs1, pp); else vs0 = fadd2(vs0, pp);
+              // systolic diagonal sums: lane l holds diagonal (key j0 + l - i) of both members
+              acc = fadd2(acc, pp);
+              if (lane == 31) {
+                dbuf[94 - i] = *reinterpret_cast<const float2*>(&acc);
+                acc = 0ull;
+              }
+              acc = __shfl_sync(0xffffffffu, acc, (lane + 31) & 31);
+            }
+          }
+          if (lane >= 1) dbuf[lane - 1] = *reinterpret_cast<const float2*>(&acc);
+          float v0a, v1a, v0b, v1b;
+          unpack_f32x2(vs0, v0a, v1a);
+          unpack_f32x2(vs1, v0b, v1b);
+          if (j < S) {
+            a.vscore[(int64_t)ctrl->slot[m0] * S + j] = (double)(v0a + v0b);
+            if (m1 < nh) a.vscore[(int64_t)ctrl->slot[m1] * S + j] = (double)(v1a + v1b);
+          }
+        } else {
+          tc_fence_before();
+          if (lane == 0) mbar_arrive(&ctrl->acc_empty[buf]);
+        }
+        named_bar_sync(1, kEpiThreads);
+        // combine: diagonal c = tile0 + cl (its key at row 0), cl in [-63, 127]; offset o = S - 64 - c.
+        // Warp-chunk wk holds the diagonals cl in [32 wk - 63, 32 wk + 31] at index cl - 32 wk + 63.
+        const float* dsum = diag + (t & 1) * (2 * 4 * 96 * 2);
+        const int et = threadIdx.x - 64;
+        for (int idx = et; idx < nh * 191; idx += kEpiThreads) {
+          const int mm = idx / 191;
+          const int cl = idx % 191 - 63;
+          double sum = 0.0;
+#pragma unroll
+          for (int wk = 0; wk < 4; ++wk) {
+            const int k = cl - 32 * wk + 63;
+            if (k >= 0 && k <= 94) sum += (double)dsum[(((mm >> 1) * 4 + wk) * 96 + k) * 2 + (mm & 1)];
+          }
+          const int cd = tile0 + cl;
+          const int o = S - kTailRows - cd;
+          if (o < 0 || o >= S) continue;
+          double* dst = a.sscore + (int64_t)ctrl->slot[mm] * S + o;
+          if (cl >= 0 && cl <= kKeys - kTailRows)
+            *dst = sum;  // the whole diagonal lies in this tile
+          else
+            atomicAdd(dst, sum);  // exactly two tiles contribute: order-free
+        }
+        // the next tile writes the other diag buffer; one barrier per tile keeps the reuse distance at 2
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Per-row combine of the chunk partials (fp64), per-head certification threshold.
+__global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs a) {
+  __shared__ int slot[kMaxMembers], head[kMaxMembers], nh_s;
+  __shared__ float amax_s[kGroupRows];
+  const int gy = blockIdx.x;
+  if (threadIdx.x == 0) nh_s = group_members(a, gy, slot, head);
+  __syncthreads();
+  const int nh = nh_s;
+  const int r = threadIdx.x;
+  const int mm = r / kTailRows;
+  const double c64 = (double)a.c_hi + (double)a.c_lo;
+  float amax = 0.f;
+  if (mm < nh) {
+    float m = -INFINITY;
+    for (int c = 0; c < a.n_chunks; ++c) {
+      const int64_t o = ((int64_t)gy * a.n_chunks + c) * kGroupRows + r;
+      if (a.st_l[o] > 0.0) m = fmaxf(m, a.st_m[o]);
+    }
+    double l = 0.0;  // st_m holds mc = fp32(m * c): rescale in the exponent domain the sums were taken in
+    for (int c = 0; c < a.n_chunks; ++c) {
+      const int64_t o = ((int64_t)gy * a.n_chunks + c) * kGroupRows + r;
+      const double lc = a.st_l[o];
+      if (lc > 0.0) l += lc * exp2((double)a.st_m[o] - (double)m);
+      amax = fmaxf(amax, a.st_amax[o]);
+    }
+    a.row_m[(int64_t)gy * kGroupRows + r] = m;
+    a.row_il[(int64_t)gy * kGroupRows + r] = (float)(1.0 / l);
+    a.row_mc[(int64_t)slot[mm] * kTailRows + (r % kTailRows)] = m;
+  }
+  amax_s[r] = amax;
+  __syncthreads();
+  if (r < nh) {
+    float mx = 0.f;
+    for (int i = 0; i < kTailRows; ++i) mx = fmaxf(mx, amax_s[r * kTailRows + i]);
+    // error model of the fp32 path: a few fp32 ulps of the largest |score| (natural-log units),
+    // relative to the probabilities; 2^-20 leaves a ~10x margin over the measured error.
+    const double smax = (double)mx * c64 * 0.6931471805599453;
+    a.tau[slot[r]] = (float)(ldexp(1.0, -20) * (1.0 + smax));
+  }
+}
+
+// Top-k (estimator.py:59-79) of the fp64 score vectors plus certification of the
+// selected set against the error threshold tau: flag the head when the
+// boundary (k-th vs (k+1)-th, the k-th vs (k-1)-th when index 0 must be forced,
+// or index 0 vs the k-th) is closer than tau * (k-th value), or the k-th value
+// ties.  One cluster of kTopkCl CTAs per vector (cluster_topk.cuh).
+constexpr int kTopkThreads = 256;
+constexpr int kTopkCl = 8;
+
+__global__ void __cluster_dims__(kTopkCl, 1, 1) __launch_bounds__(kTopkThreads)
+    vs_topk_certify_kernel(const double* __restrict__ vscore, const double* __restrict__ sscore, int S, int k_v,
+                           int k_s, const float* __restrict__ tau, int32_t* __restrict__ vert_out,
+                           int32_t* __restrict__ slash_out, int32_t* __restrict__ uncertain) {
+  using TK = ClusterTopK<kTopkThreads, kTopkCl>;
+  __shared__ typename TK::Storage sm;
+  const int hi = blockIdx.y;
+  if (blockIdx.z == 0)
+    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, false, vert_out + (int64_t)hi * k_v, tau + hi, uncertain + hi);
+  else
+    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, true, slash_out + (int64_t)hi * k_s, tau + hi, uncertain + hi);
+}
+
+template <int kD>
+int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv, int S, const int32_t* head_ids,
+                 int n_heads, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
+                 int32_t* uncertain, uint8_t* ws, cudaStream_t st) {
+  using L = TcLayout<kD>;
+  TcArgs a{};
+  a.S = S;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.hpk = Hq / Hkv;
+  a.gpk = (a.hpk + kMaxMembers - 1) / kMaxMembers;
+  a.n_heads = n_heads;
+  a.head_ids = head_ids;
+  a.n_tiles = (S + kKeys - 1) / kKeys;
+  const int n_groups = Hkv * a.gpk;
+  // active groups are at most min(n_groups, ceil(n_heads/1)); size chunks for ~one CTA per SM
+  const int active = min(n_groups, n_heads);
+  a.n_chunks = max(1, min(a.n_tiles, 148 / active));  // one wave: at most one CTA per SM
+  const double c64 = 1.4426950408889634 / sqrt((double)kD);
+  a.c_hi = (float)c64;
+  a.c_lo = (float)(c64 - (double)a.c_hi);
+  auto take = [&](size_t bytes) {
+    uint8_t* p = ws;
+    ws += (bytes + 255) & ~size_t(255);
+    return p;
+  };
+  const size_t part = (size_t)n_groups * a.n_chunks * kGroupRows;
+  a.st_m = reinterpret_cast<float*>(take(part * 4));
+  a.st_l = reinterpret_cast<double*>(take(part * 8));
+  a.st_amax = reinterpret_cast<float*>(take(part * 4));
+  a.row_m = reinterpret_cast<float*>(take((size_t)n_groups * kGroupRows * 4));
+  a.row_il = reinterpret_cast<float*>(take((size_t)n_groups * kGroupRows * 4));
+  a.tau = reinterpret_cast<float*>(take((size_t)n_heads * 4));
+  a.vscore = vscore ? vscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
+  a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
+  a.tile_max = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * a.n_tiles * 4));
+  a.row_mc = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * 4));
+  int32_t* flags_ws = reinterpret_cast<int32_t*>(take((size_t)n_heads * 4));
+
+  CUtensorMap tq, tk;
+  int rc;
+  if ((rc = make_tmap_bf16_3d(&tq, q, kD, S, Hq, kTailRows))) return rc;
+  if ((rc = make_tmap_bf16_3d(&tk, k, kD, S, Hkv, kKeys))) return rc;
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[kD / 64 - 1]) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(vs_tc_kernel<kD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              L::kSmem), "vs_tc smem attr")))
+      return rc;
+    if ((rc = check_cuda(cudaFuncSetAttribute(vs_tc_kernel<kD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              L::kSmem), "vs_tc smem attr")))
+      return rc;
+    attr_done[kD / 64 - 1] = true;
+  }
+  if ((rc = check_cuda(cudaMemsetAsync(a.sscore, 0, (size_t)n_heads * S * 8, st), "memset slash"))) return rc;
+  if (uncertain && (rc = check_cuda(cudaMemsetAsync(uncertain, 0, (size_t)n_heads * 4, st), "memset flags")))
+    return rc;
+  int32_t* flags = uncertain ? uncertain : flags_ws;
+  if (!uncertain && (rc = check_cuda(cudaMemsetAsync(flags, 0, (size_t)n_heads * 4, st), "memset flags"))) return rc;
+  const dim3 grid((unsigned)a.n_chunks, (unsigned)n_groups);
+  note_launches(4);  // pass 1, combine, pass 2, top-k
+  vs_tc_kernel<kD, 1><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
+  if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 1"))) return rc;
+  vs_tc_combine_kernel<<<n_groups, kGroupRows, 0, st>>>(a);
+  vs_tc_kernel<kD, 2><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
+  if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 2"))) return rc;
+  vs_topk_certify_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
+                                                                                        k_s, a.tau, vout, sout, flags);
+  if ((rc = check_cuda(cudaGetLastError(), "vs_tc top-k"))) return rc;
+  // uncertified heads: fp64 re-estimation in the same stream (no host sync), skipping the
+  // tiles whose probabilities round to exactly 0
+  return vs_exact_run(SPF_DTYPE_BF16, q, k, Hq, Hkv, S, kD, head_ids, n_heads, kTailRows, k_v, k_s, vout, sout,
+                      a.vscore, a.sscore, flags, a.tile_max, a.row_mc, ws, st);
+}
+
+}  // namespace
+
+bool vs_fast_supported(int dtype, int head_dim, int seq_len, int last_q) {
+  return dtype == SPF_DTYPE_BF16 && (head_dim == 64 || head_dim == 128) && last_q == kTailRows &&
+         seq_len >= kTailRows;
+}
+
+size_t vs_fast_workspace_size(int n_q_heads, int n_kv_heads, int n_heads, int seq_len) {
+  const size_t hpk = n_q_heads / max(1, n_kv_heads);
+  const size_t n_groups = (size_t)n_kv_heads * ((hpk + kMaxMembers - 1) / kMaxMembers);
+  const size_t n_tiles = (seq_len + kKeys - 1) / kKeys;
+  const size_t n_chunks = std::max<size_t>(1, std::min<size_t>(n_tiles, 148));
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t part = n_groups * n_chunks * kGroupRows;
+  return al(part * 4) + al(part * 8) + al(part * 4) + 2 * al(n_groups * kGroupRows * 4) + al(n_heads * 4) +
+         2 * al((size_t)n_heads * seq_len * 8) + al((size_t)n_heads * kTailRows * n_tiles * 4) +
+         al((size_t)n_heads * kTailRows * 4) + al(n_heads * 4) + vs_exact_workspace_size(n_heads, seq_len, kTailRows);
+}
+
+int vs_estimate_fast(const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
+                     int n_heads, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
+                     int32_t* uncertain, void* workspace, cudaStream_t st) {
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const auto* qb = reinterpret_cast<const __nv_bfloat16*>(q);
+  const auto* kb = reinterpret_cast<const __nv_bfloat16*>(k);
+  if (d == 128)
+    return vs_fast_impl<128>(qb, kb, Hq, Hkv, S, head_ids, n_heads, k_v, k_s, vout, sout, vscore, sscore, uncertain,
+                             ws, st);
+  return vs_fast_impl<64>(qb, kb, Hq, Hkv, S, head_ids, n_heads, k_v, k_s, vout, sout, vscore, sscore, uncertain, ws,
+                          st);
+}
+
+}  // namespace spf

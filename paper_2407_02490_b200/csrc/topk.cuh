@@ -57,9 +57,22 @@ struct BlockTopK {
       const Key dmask = (Key)((1u << width) - 1);
       for (int i = tid; i < kBins; i += kThreads) sm.hist[i] = 0;
       __syncthreads();
-      for (int i = tid; i < n; i += kThreads) {
-        const Key key = mono_key(vals[i]);
-        if ((key & pmask) == prefix) atomicAdd(&sm.hist[(int)((key >> sh) & dmask)], 1);
+      // warp-aggregated histogram: the leading digits are highly concentrated (values of one
+      // exponent), so lanes with equal digits are merged before the shared-memory atomic
+      for (int base = 0; base < n; base += kThreads) {
+        const int i = base + tid;
+        bool hit = false;
+        int dig = 0;
+        if (i < n) {
+          const Key key = mono_key(vals[i]);
+          hit = (key & pmask) == prefix;
+          dig = (int)((key >> sh) & dmask);
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const unsigned peers = __match_any_sync(act, dig);
+          if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sm.hist[dig], __popc(peers));
+        }
       }
       __syncthreads();
       // suffix counts: reverse-order inclusive scan over bins (each thread owns kBins/kThreads bins)

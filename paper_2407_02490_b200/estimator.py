@@ -7,9 +7,12 @@ Drop-in mirror of /root/reference/pkg/src/sparseprefill/estimator.py:
 * ``argtopk`` (59-67): stable descending order, ties to the lower index;
 * ``estimate_vertical_slash(q, k, cfg)`` (82-114) and
   ``estimate_block_sparse(q, k, cfg)`` (117-143) take NumPy [S, d] arrays
-  like the reference and run libspf's fp64-exact estimation kernels
-  (spf_vs_estimate / spf_bs_estimate), so the selected index sets are those
-  of the reference.
+  like the reference (fp32) and run libspf's fp64 estimation kernels
+  (spf_vs_estimate mode SPF_VS_EXACT / spf_bs_estimate), so the selected
+  index sets are those of the reference.  bf16 device tensors (the production
+  path) use the tensor-core VS estimator whose selections are certified per
+  head against its error model; uncertified heads are re-run on the fp64
+  path.
 
 ``estimate_vertical_slash_gpu`` / ``estimate_block_sparse_gpu`` are the
 batched multi-head (GQA) device entries used by ``prefill.py``.
@@ -84,13 +87,15 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise TypeError("q/k must be bf16 or fp32")
 
 
-def estimate_vertical_slash_gpu(q: torch.Tensor, k: torch.Tensor, cfg: VerticalSlash, head_ids=None,
-                                with_scores: bool = False, stream=None):
-    """Batched VS estimation: q [Hq, S, d], k [Hkv, S, d] (bf16/fp32).
+def vs_estimate_async(q: torch.Tensor, k: torch.Tensor, cfg: VerticalSlash, head_ids=None, mode: str = "fast",
+                      with_scores: bool = False, stream=None):
+    """One stream-ordered spf_vs_estimate call (no host sync).
 
-    Returns (vertical [n, min(k_v, S)] int32 ascending, slash [n, min(k_s, S)]
-    int32 descending[, vscore, sscore fp64 [n, S]]) for the heads in
-    ``head_ids`` (int32 device tensor; None = all q-heads).
+    Returns (vertical, slash, vscore, sscore, uncertain): vertical
+    [n, min(k_v, S)] int32 ascending, slash [n, min(k_s, S)] int32 descending,
+    fp64 score vectors [n, S] (or None) and the per-head int32 flags of the
+    tensor-core path (1 = the selection was too close to certify and the head
+    was re-estimated on the fp64 path inside the same call).
     """
     dev = _dev.require_cuda(q.device)
     hq, s_len, d = q.shape
@@ -103,13 +108,30 @@ def estimate_vertical_slash_gpu(q: torch.Tensor, k: torch.Tensor, cfg: VerticalS
     sl = torch.empty((n, ks), dtype=torch.int32, device=dev)
     vsc = torch.empty((n, s_len), dtype=torch.float64, device=dev) if with_scores else None
     ssc = torch.empty((n, s_len), dtype=torch.float64, device=dev) if with_scores else None
+    flags = torch.empty(n, dtype=torch.int32, device=dev)
+    code = _lib.SPF_VS_FAST if mode == "fast" else _lib.SPF_VS_EXACT
+    dt = _dtype_code(q)
     lib = _lib.load()
-    ws_bytes = lib.spf_vs_estimate_workspace_size(n, s_len, cfg.last_q)
+    ws_bytes = lib.spf_vs_estimate_workspace_size(code, dt, hq, hkv, n, s_len, d, cfg.last_q)
     ws = _dev.workspace(ws_bytes, dev)
-    _lib.check(lib.spf_vs_estimate(_dtype_code(q), _dev.ptr(q.contiguous()), _dev.ptr(k.contiguous()), hq, hkv,
-                                   s_len, d, _dev.ptr(head_ids), n, cfg.last_q, cfg.k_v, cfg.k_s, _dev.ptr(vert),
-                                   _dev.ptr(sl), _dev.ptr(vsc), _dev.ptr(ssc), _dev.ptr(ws), ws_bytes,
+    _lib.check(lib.spf_vs_estimate(code, dt, _dev.ptr(q.contiguous()), _dev.ptr(k.contiguous()), hq, hkv, s_len, d,
+                                   _dev.ptr(head_ids), n, cfg.last_q, cfg.k_v, cfg.k_s, _dev.ptr(vert), _dev.ptr(sl),
+                                   _dev.ptr(vsc), _dev.ptr(ssc), _dev.ptr(flags), _dev.ptr(ws), ws_bytes,
                                    _dev.stream_handle(stream)), "spf_vs_estimate")
+    return vert, sl, vsc, ssc, flags
+
+
+def estimate_vertical_slash_gpu(q: torch.Tensor, k: torch.Tensor, cfg: VerticalSlash, head_ids=None,
+                                with_scores: bool = False, stream=None, mode: str = "fast"):
+    """Batched VS estimation: q [Hq, S, d], k [Hkv, S, d] (bf16/fp32).
+
+    Returns (vertical [n, min(k_v, S)] int32 ascending, slash [n, min(k_s, S)]
+    int32 descending[, vscore, sscore fp64 [n, S]]) for the heads in
+    ``head_ids`` (int32 device tensor; None = all q-heads).  ``mode="fast"``
+    runs the tensor-core path (uncertified heads are re-run on the fp64 path
+    in the same stream); ``mode="exact"`` runs the fp64 path only.
+    """
+    vert, sl, vsc, ssc, _ = vs_estimate_async(q, k, cfg, head_ids, mode, with_scores, stream)
     if with_scores:
         return vert, sl, vsc, ssc
     return vert, sl

@@ -6,6 +6,9 @@ config JSON v1 of patterns.py:236-266), the hot path of the reference's
 ``run_head`` (sparse_attn.py:67-94) for every head at once:
 
   1. online estimation      VS heads grouped by (k_v, k_s, last_q): spf_vs_estimate
+                            on the tensor cores; heads whose top-k boundary is
+                            too close for its error model are re-run on the
+                            fp64 path inside the same stream-ordered call
   2. index compaction       per-row counts for VS / A-shape / BS heads -> one
                             CSR over all q-heads (spf_*_layout_count,
                             spf_csr_offsets, spf_*_layout_fill); BS heads'
@@ -26,7 +29,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _dev, kernels, layouts
-from .estimator import estimate_block_sparse_gpu, estimate_vertical_slash_gpu
+from .estimator import estimate_block_sparse_gpu, vs_estimate_async
 from .patterns import AShape, BlockSparse, HeadPatternConfig, VerticalSlash, n_block_rows
 
 
@@ -92,7 +95,7 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
     vs_sel = {}
     for cfg, ids, m in groups:
         if isinstance(cfg, VerticalSlash):
-            vert, sl = estimate_vertical_slash_gpu(q, k, cfg, ids, stream=stream)
+            vert, sl, _, _, _ = vs_estimate_async(q, k, cfg, ids, mode="fast", stream=stream)
             vs_sel[cfg] = (vert, sl)
             layouts.vs_count(vert, sl, ids, s_len, block_size, tc, cc, stream)
         elif isinstance(cfg, AShape):

@@ -40,11 +40,47 @@ def test_vs_golden_scores_and_bf16_path(golden, P):
         q, k, _ = gaussian_qkv(s, d, seed, True)
         tq = torch.from_numpy(q).cuda().to(torch.bfloat16)[None]
         tk = torch.from_numpy(k).cuda().to(torch.bfloat16)[None]
-        vert, sl, vsc, ssc = P.estimate_vertical_slash_gpu(tq, tk, P.VerticalSlash(kv, ks, lq), with_scores=True)
+        cfg = P.VerticalSlash(kv, ks, lq)
+        # fp64 path: scores equal to the reference's to ~1 ulp
+        vert, sl, vsc, ssc = P.estimate_vertical_slash_gpu(tq, tk, cfg, with_scores=True, mode="exact")
         np.testing.assert_array_equal(vert[0].cpu().numpy(), golden[f"{name}__vertical"], err_msg=name)
         np.testing.assert_array_equal(sl[0].cpu().numpy(), golden[f"{name}__slash"], err_msg=name)
         np.testing.assert_allclose(vsc[0].cpu().numpy(), golden[f"{name}__vscore"], rtol=1e-12, atol=0)
         np.testing.assert_allclose(ssc[0].cpu().numpy(), golden[f"{name}__sscore"], rtol=1e-12, atol=0)
+        # production path (tensor cores + certification / exact re-run): same index sets
+        vert, sl = P.estimate_vertical_slash_gpu(tq, tk, cfg, mode="fast")
+        np.testing.assert_array_equal(vert[0].cpu().numpy(), golden[f"{name}__vertical"], err_msg=name)
+        np.testing.assert_array_equal(sl[0].cpu().numpy(), golden[f"{name}__slash"], err_msg=name)
+
+
+@pytest.mark.parametrize("s,seed,gen", [(8192, 0, "iid"), (8192, 3, "iid"), (32768, 1, "iid"), (5000, 2, "iid"),
+                                        (16384, 0, "local"), (131072, 0, "local")])
+def test_vs_tensor_core_error_model(P, s, seed, gen):
+    """The tensor-core scores stay well inside the certification threshold
+    (tau = 2^-20 (1 + max|s|), estimate_vs_tc.cu): measured max relative error
+    of the vertical / slash vectors vs the fp64 path, on all four heads of a
+    GQA group (Hq=4, Hkv=1)."""
+    from benchmarks.workloads import g_iid_qkv, g_local_qkv
+
+    gen_fn = g_iid_qkv if gen == "iid" else g_local_qkv
+    q, k, _ = gen_fn(4, 1, s, 128, seed=seed, device="cuda")
+    cfg = P.VerticalSlash(1000, 6096, 64)
+    from paper_2407_02490_b200.estimator import vs_estimate_async
+
+    vf, sf, vsf, ssf, flags = vs_estimate_async(q, k, cfg, mode="fast", with_scores=True)
+    ve, se, vse, sse, _ = vs_estimate_async(q, k, cfg, mode="exact", with_scores=True)
+    qf = q.float()
+    smax = (qf[:, -64:] @ k[0].float().T).abs().max().item() / np.sqrt(128)
+    tau = 2.0 ** -20 * (1 + smax)
+    for fast, exact in ((vsf, vse), (ssf, sse)):
+        fast, exact = fast.cpu().numpy(), exact.cpu().numpy()
+        big = exact > 1e-20
+        rel = np.abs(fast[big] - exact[big]) / exact[big]
+        assert rel.max() < tau / 2, (gen, s, rel.max(), tau)
+    # certified heads select exactly the fp64 sets
+    for h in range(4):
+        if int(flags[h]) == 0:
+            assert torch.equal(vf[h], ve[h]) and torch.equal(sf[h], se[h]), h
 
 
 def test_vs_gqa_multihead_matches_port(P):

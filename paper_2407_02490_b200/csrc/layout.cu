@@ -20,97 +20,155 @@ namespace spf {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kSmemIdx = 11 * 1024;  // ints staged in smem when the head's lists fit (44 KB)
+constexpr int kSmemIdx = 24 * 1024;  // ints staged in smem when the head's lists + gap list fit (96 KB)
 
 __device__ __forceinline__ int head_of(const int32_t* head_ids, int i) { return head_ids ? head_ids[i] : i; }
 
-// One row of the VS merge.  kFill=false: counts only.
-template <bool kFill>
-__device__ void vs_merge_row(const int32_t* __restrict__ pts, int np, const int32_t* __restrict__ sl, int ns, int r,
-                             int S, int B, int32_t* __restrict__ tiles, int32_t* __restrict__ cols, int64_t& nt,
-                             int64_t& nc) {
-  const int q_start = r * B;
-  const int q_end = min(q_start + B, S);
-  int jv = 0;
-  int64_t t = 0, c = 0;
-  bool have = false;
-  int cs = 0, ce = 0;
-  auto flush = [&](int fs, int fe) {
-    const int cover = fs + ((fe - fs + B - 1) / B) * B;
-    while (jv < np && pts[jv] < cover) {
-      const int x = pts[jv];
-      if (x < fs) {
-        if (kFill) cols[c] = x;
-        ++c;
-      }
-      ++jv;
-    }
-    for (int s = fs; s < fe; s += B) {
-      if (kFill) tiles[t] = s;
-      ++t;
-    }
-  };
-  for (int i = 0; i < ns; ++i) {
-    const int o = sl[i];
-    if (o >= q_end) continue;  // diagonal left of key 0 for this row (vs_index.py:71-72)
-    const int rs = max(0, q_start - o);
-    const int re = q_end - o;
-    if (!have) {
-      cs = rs;
-      ce = re;
-      have = true;
-    } else if (rs <= ce || rs < cs + ((ce - cs + B - 1) / B) * B) {
-      ce = max(ce, re);
-    } else {
-      flush(cs, ce);
-      cs = rs;
-      ce = re;
-    }
-  }
-  if (have) flush(cs, ce);
-  for (; jv < np; ++jv) {  // trailing points right of every range (vs_index.py:85-90)
-    const int x = pts[jv];
-    if (x < q_end) {
-      if (kFill) cols[c] = x;
-      ++c;
-    }
-  }
-  nt = t;
-  nc = c;
-}
+// Vertical-Slash point-range merge (Alg. 4, vs_index.py:44-94), one warp per
+// query-block row, bit-exact with the reference's sequential loop.  The slash
+// ranges of a row have non-decreasing starts and increasing ends, so a range
+// can only end the current group where it starts past the previous range's
+// end (a "gap"); gap lanes of each 32-range batch are resolved in order with
+// the exact coalescing rule of vs_index.py:78, all other ranges merge.  The
+// vertical points consumed by a flush are classified (column if < group
+// start, else absorbed) 32 at a time with ballots.
+constexpr int kMergeWarps = 8;
 
 template <bool kFill>
-__global__ void __launch_bounds__(kThreads) vs_merge_kernel(const int32_t* __restrict__ vertical, int n_v,
-                                                            const int32_t* __restrict__ slash, int n_s,
-                                                            const int32_t* __restrict__ head_ids, int S, int B,
-                                                            int64_t* __restrict__ tile_cnt,
-                                                            int64_t* __restrict__ col_cnt,
-                                                            const int64_t* __restrict__ tile_off,
-                                                            const int64_t* __restrict__ col_off,
-                                                            int32_t* __restrict__ tiles, int32_t* __restrict__ cols) {
+__global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
+    const int32_t* __restrict__ vertical, int n_v, const int32_t* __restrict__ slash, int n_s,
+    const int32_t* __restrict__ head_ids, int S, int B, int rows_per_cta, int64_t* __restrict__ tile_cnt,
+    int64_t* __restrict__ col_cnt, const int64_t* __restrict__ tile_off, const int64_t* __restrict__ col_off,
+    int32_t* __restrict__ tiles, int32_t* __restrict__ cols) {
   extern __shared__ int32_t s_idx[];
+  __shared__ int s_ngap;
   const int i = blockIdx.y;
   const int h = head_of(head_ids, i);
   const int n_rows = (S + B - 1) / B;
   const int32_t* pts = vertical + (int64_t)i * n_v;
   const int32_t* sl = slash + (int64_t)i * n_s;
-  if (n_v + n_s <= kSmemIdx) {
+  const bool staged = n_v + 2 * n_s <= kSmemIdx;
+  int32_t* gaps = s_idx + n_v + n_s;
+  if (staged) {
     for (int j = threadIdx.x; j < n_v; j += blockDim.x) s_idx[j] = pts[j];
     for (int j = threadIdx.x; j < n_s; j += blockDim.x) s_idx[n_v + j] = sl[j];
     __syncthreads();
     pts = s_idx;
     sl = s_idx + n_v;
+    // gap list: slash indices j whose range starts past the previous range's end in every
+    // full row (o[j-1] - o[j] > B); only these can end a coalesced group
+    if (threadIdx.x < 32) {
+      const int ln = threadIdx.x;
+      int n = 0;
+      for (int b0 = 1; b0 < n_s; b0 += 32) {
+        const int j = b0 + ln;
+        const bool g = j < n_s && sl[j - 1] - sl[j] > B;
+        const unsigned m = __ballot_sync(0xffffffffu, g);
+        if (g) gaps[n + __popc(m & ((1u << ln) - 1u))] = j;
+        n += __popc(m);
+      }
+      if (ln == 0) s_ngap = n;
+    }
+    __syncthreads();
   }
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
-  const int64_t row = (int64_t)h * n_rows + r;
-  int64_t nt, nc;
-  if (kFill) {
-    vs_merge_row<true>(pts, n_v, sl, n_s, r, S, B, tiles + tile_off[row], cols + col_off[row], nt, nc);
-  } else {
-    vs_merge_row<false>(pts, n_v, sl, n_s, r, S, B, nullptr, nullptr, nt, nc);
-    tile_cnt[row] = nt;
-    col_cnt[row] = nc;
+  const int n_gap = staged ? s_ngap : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int r_end = min(n_rows, (blockIdx.x + 1) * rows_per_cta);
+  for (int r = blockIdx.x * rows_per_cta + warp; r < r_end; r += kMergeWarps) {
+    const int64_t row = (int64_t)h * n_rows + r;
+    const int q_start = r * B, q_end = min(q_start + B, S);
+    int32_t* tout = kFill ? tiles + tile_off[row] : nullptr;
+    int32_t* cout = kFill ? cols + col_off[row] : nullptr;
+    int64_t nt = 0, nc = 0;
+    int jv = 0;
+    // flush a group [fs, fe): points < its cover end are consumed (columns if < fs), then its tiles
+    auto flush = [&](int fs, int fe, bool with_tiles) {
+      const int cover = with_tiles ? fs + ((fe - fs + B - 1) / B) * B : fe;
+      while (true) {
+        const int idx = jv + lane;
+        const int x = idx < n_v ? pts[idx] : INT_MAX;
+        const bool in = x < cover;  // ascending points: a lane prefix
+        const unsigned m_in = __ballot_sync(0xffffffffu, in);
+        const bool is_col = in && x < fs;
+        const unsigned m_col = __ballot_sync(0xffffffffu, is_col);
+        if (kFill && is_col) cout[nc + __popc(m_col & lt)] = x;
+        nc += __popc(m_col);
+        jv += __popc(m_in);
+        if (m_in != 0xffffffffu) break;
+      }
+      if (with_tiles) {
+        const int ntile = (fe - fs + B - 1) / B;
+        if (kFill)
+          for (int t = lane; t < ntile; t += 32) tout[nt + t] = fs + t * B;
+        nt += ntile;
+      }
+    };
+    // slashes are descending: skip the prefix with o >= q_end (vs_index.py:71-72)
+    int lo = 0, hi = n_s;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sl[mid] >= q_end) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n_s && staged && q_end - q_start == B) {
+      // full row: visit only the gap candidates after lo (the other ranges always coalesce)
+      int cs = max(0, q_start - sl[lo]);
+      int g0 = 0, g1 = n_gap;
+      while (g0 < g1) {
+        const int mid = (g0 + g1) >> 1;
+        if (gaps[mid] <= lo) g0 = mid + 1;
+        else g1 = mid;
+      }
+      for (int base = g0; base < n_gap; base += 32) {
+        const int idx = base + lane;
+        const bool valid = idx < n_gap;
+        const int j = valid ? gaps[idx] : 1;
+        const int rs = max(0, q_start - sl[j]);
+        const int pre = q_end - sl[j - 1];
+        unsigned cand = __ballot_sync(0xffffffffu, valid && rs > pre);
+        while (cand) {
+          const int l = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int rs_l = __shfl_sync(0xffffffffu, rs, l);
+          const int pre_l = __shfl_sync(0xffffffffu, pre, l);
+          if (rs_l >= cs + ((pre_l - cs + B - 1) / B) * B) {
+            flush(cs, pre_l, true);
+            cs = rs_l;
+          }
+        }
+      }
+      flush(cs, q_end - sl[n_s - 1], true);
+    } else if (lo < n_s) {
+      int cs = max(0, q_start - sl[lo]);
+      int ce = q_end - sl[lo];
+      for (int base = lo + 1; base < n_s; base += 32) {
+        const int idx = base + lane;
+        const bool valid = idx < n_s;
+        const int o = valid ? sl[idx] : 0;
+        const int rs = max(0, q_start - o), re = q_end - o;
+        int prev_re = __shfl_up_sync(0xffffffffu, re, 1);
+        if (lane == 0) prev_re = ce;
+        unsigned cand = __ballot_sync(0xffffffffu, valid && rs > prev_re);
+        while (cand) {
+          const int l = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int rs_l = __shfl_sync(0xffffffffu, rs, l);
+          const int pre = __shfl_sync(0xffffffffu, prev_re, l);  // current group end
+          if (rs_l >= cs + ((pre - cs + B - 1) / B) * B) {      // not coalesced (vs_index.py:78)
+            flush(cs, pre, true);
+            cs = rs_l;
+          }
+        }
+        ce = __shfl_sync(0xffffffffu, re, min(31, n_s - 1 - base));
+      }
+      flush(cs, ce, true);
+    }
+    flush(q_end, q_end, false);  // trailing points < q_end become columns (vs_index.py:85-90)
+    if (!kFill && lane == 0) {
+      tile_cnt[row] = nt;
+      col_cnt[row] = nc;
+    }
   }
 }
 
@@ -185,6 +243,17 @@ __global__ void area_kernel(int S, int B, const int32_t* __restrict__ tiles, con
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(area + h, (unsigned long long)acc);
 }
 
+// rows per CTA for the warp-per-row merge: about 4 CTAs per SM over all heads, >= 8 rows
+int merge_rows_per_cta(int S, int B, int n_heads) {
+  const int n_rows = (S + B - 1) / B;
+  const int ctas_per_head = max(1, (148 * 4) / max(1, n_heads));
+  return max(kMergeWarps, (n_rows + ctas_per_head - 1) / ctas_per_head);
+}
+dim3 merge_grid(int S, int B, int n_heads, int rpc) {
+  const int n_rows = (S + B - 1) / B;
+  return dim3((unsigned)((n_rows + rpc - 1) / rpc), (unsigned)n_heads);
+}
+
 dim3 row_grid(int S, int B, int n_heads) { return dim3((unsigned)(((S + B - 1) / B + kThreads - 1) / kThreads), (unsigned)n_heads); }
 
 }  // namespace
@@ -228,12 +297,17 @@ int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, 
                         void* stream) {
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
-  const size_t smem = (n_v + n_s <= kSmemIdx) ? (size_t)(n_v + n_s) * 4 : 0;
+  const size_t smem = (n_v + 2 * n_s <= kSmemIdx) ? (size_t)(n_v + 2 * n_s) * 4 : 0;
+  const int rpc = merge_rows_per_cta(seq_len, block_size, n_heads);
+  int rc;
+  if ((rc = check_cuda(cudaFuncSetAttribute(vs_merge_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmemIdx * 4), "merge smem attr")))
+    return rc;
   note_launches(1);
-  vs_merge_kernel<false><<<row_grid(seq_len, block_size, n_heads), kThreads, smem,
-                           reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
-                                                                     block_size, tile_counts, col_counts, nullptr,
-                                                                     nullptr, nullptr, nullptr);
+  vs_merge_warp_kernel<false><<<merge_grid(seq_len, block_size, n_heads, rpc), kMergeWarps * 32, smem,
+                                reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
+                                                                          block_size, rpc, tile_counts, col_counts,
+                                                                          nullptr, nullptr, nullptr, nullptr);
   return check_cuda(cudaGetLastError(), "vs_layout_count");
 }
 
@@ -242,12 +316,18 @@ int spf_vs_layout_fill(const int32_t* vertical, int n_v, const int32_t* slash, i
                        const int64_t* col_offsets, int32_t* tile_starts, int32_t* col_indices, void* stream) {
   if (block_size < 1) return set_error(SPF_ERR_INVALID, "block_size must be >= 1");
   if (n_heads <= 0 || seq_len <= 0) return SPF_OK;
-  const size_t smem = (n_v + n_s <= kSmemIdx) ? (size_t)(n_v + n_s) * 4 : 0;
+  const size_t smem = (n_v + 2 * n_s <= kSmemIdx) ? (size_t)(n_v + 2 * n_s) * 4 : 0;
+  const int rpc = merge_rows_per_cta(seq_len, block_size, n_heads);
+  int rc;
+  if ((rc = check_cuda(cudaFuncSetAttribute(vs_merge_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmemIdx * 4), "merge smem attr")))
+    return rc;
   note_launches(1);
-  vs_merge_kernel<true><<<row_grid(seq_len, block_size, n_heads), kThreads, smem,
-                          reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
-                                                                    block_size, nullptr, nullptr, tile_offsets,
-                                                                    col_offsets, tile_starts, col_indices);
+  vs_merge_warp_kernel<true><<<merge_grid(seq_len, block_size, n_heads, rpc), kMergeWarps * 32, smem,
+                               reinterpret_cast<cudaStream_t>(stream)>>>(vertical, n_v, slash, n_s, head_ids, seq_len,
+                                                                         block_size, rpc, nullptr, nullptr,
+                                                                         tile_offsets, col_offsets, tile_starts,
+                                                                         col_indices);
   return check_cuda(cudaGetLastError(), "vs_layout_fill");
 }
 

@@ -86,6 +86,33 @@ def test_large_merge_matches_c_oracle(P, rng):
     np.testing.assert_array_equal(c, wc)
 
 
+@pytest.mark.parametrize("kind", ["band", "spaced_b", "spaced_b1", "clustered"])
+def test_structured_merges_match_c_oracle(P, rng, kind):
+    """Slash patterns that stress the coalescing rule of the warp-parallel
+    merge: one contiguous band (G-local), offsets exactly B and B+1 apart
+    (every range a gap candidate, half of them coalesced by the cover rule),
+    and clustered offsets."""
+    s_len, b = 65536 + 37, 64
+    if kind == "band":
+        slash = np.arange(6095, -1, -1)
+    elif kind == "spaced_b":
+        slash = np.arange(0, 64 * 900, 64)[::-1]
+    elif kind == "spaced_b1":
+        slash = np.arange(0, 65 * 900, 65)[::-1]
+    else:
+        centers = rng.choice(s_len - 200, size=60, replace=False)
+        slash = np.unique((centers[:, None] + rng.integers(0, 150, size=(60, 40))).ravel())[::-1]
+    slash = slash[slash < s_len]
+    vertical = np.sort(rng.choice(s_len, size=1000, replace=False))
+    layout = P.build_vs_layout(P.VSIndices(vertical=vertical, slash=slash), s_len, b)
+    t, to, c, co = layout.csr()
+    wt, wto, wc, wco = port.build_vs_csr(vertical, slash, s_len, b)
+    np.testing.assert_array_equal(to, wto)
+    np.testing.assert_array_equal(t, wt)
+    np.testing.assert_array_equal(co, wco)
+    np.testing.assert_array_equal(c, wc)
+
+
 def test_ashape_golden_and_random(golden, P, rng):
     names = sorted({k.split("__")[0] for k in golden.files if k.startswith("as_")})
     for name in names:

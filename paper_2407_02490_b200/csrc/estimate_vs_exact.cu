@@ -68,7 +68,10 @@ struct ExSmem {
   float P[kRowT][kKeyT + 1];
 };
 
-// acc[4][4] = q_tail rows (r0 + 4 tr + a) . keys (k0 + 4 tk + b), fp64, d ascending
+// acc[a][b] = q_tail row (r0 + 4 tr + a) . key (k0 + tk + 16 b), fp64, d ascending.
+// Keys are strided by 16 across a thread's four columns so one warp-wide LDS.64
+// of the key chunk reads 16 consecutive doubles (one wavefront, no conflicts);
+// the row operand is a 2-address broadcast.
 template <typename T>
 __device__ void score_tile(ExSmem& sm, const T* qh, const T* kh, int r0, int n_rows_valid, int k0, int S, int d,
                            double (&acc)[4][4]) {
@@ -87,13 +90,14 @@ __device__ void score_tile(ExSmem& sm, const T* qh, const T* kh, int r0, int n_r
     }
     __syncthreads();
     const int cn = min(kDc, d - c0);
+#pragma unroll 4
     for (int c = 0; c < cn; ++c) {
       const double2 qa = *reinterpret_cast<const double2*>(sm.At + c * kLd + 4 * tr);
       const double2 qb = *reinterpret_cast<const double2*>(sm.At + c * kLd + 4 * tr + 2);
-      const double2 ka = *reinterpret_cast<const double2*>(sm.Bt + c * kLd + 4 * tk);
-      const double2 kb = *reinterpret_cast<const double2*>(sm.Bt + c * kLd + 4 * tk + 2);
       const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-      const double kv[4] = {ka.x, ka.y, kb.x, kb.y};
+      double kv[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) kv[b] = sm.Bt[c * kLd + tk + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -117,7 +121,7 @@ __device__ bool item_significant(const ExArgs& a, int h, int k0) {
 }
 
 template <typename T, int kPass>
-__global__ void __launch_bounds__(kThreads) vs_exact_kernel(const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                             const ExArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   ExSmem& sm = *reinterpret_cast<ExSmem*>(smraw);
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) vs_exact_kernel(const T* __restrict_
             double mx = -INFINITY;
 #pragma unroll
             for (int y = 0; y < 4; ++y) {
-              const int j = kk0 + 4 * tk + y;
+              const int j = kk0 + tk + 16 * y;
               const bool valid = i < L && j <= abs_i;  // abs_i < S
               s[y] = valid ? a.scale * acc[x][y] : -INFINITY;
               mx = fmax(mx, s[y]);
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) vs_exact_kernel(const T* __restrict_
 #pragma unroll
               for (int y = 0; y < 4; ++y) {
                 const float p = (s[y] == -INFINITY) ? 0.f : __double2float_rn(exp(s[y] - mrow[x]) / ilrow[x]);
-                sm.P[4 * tr + x][4 * tk + y] = p;
+                sm.P[4 * tr + x][tk + 16 * y] = p;
               }
             }
           }

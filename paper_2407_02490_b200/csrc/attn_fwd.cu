@@ -38,7 +38,6 @@ namespace {
 
 constexpr int kRows = 128;   // query rows per CTA
 constexpr int kBox = 64;     // keys per step
-constexpr int kStages = 2;   // K/V stages
 constexpr int kThreads = 192;
 
 enum : int { kTile = 0, kChip = 1, kEnd = 2 };
@@ -52,17 +51,30 @@ struct StepDesc {
   int pmax[kBox];  // chip: running max of the chip's keys (prefix rule)
 };
 
+// Ring depths: K is loaded one step ahead of V and released as soon as its
+// QK^T completes, so it gets the deeper ring; V (and the step descriptor that
+// travels with it) is released after PV.
+template <bool kSplit>
+struct Rings {
+  static constexpr int kK = kSplit ? 2 : 3;
+  static constexpr int kV = 2;
+};
+
+template <bool kSplit>
 struct Ctrl {
   uint64_t q_full;
-  uint64_t kv_full[kStages];
-  uint64_t kv_empty[kStages];
+  uint64_t k_full[Rings<kSplit>::kK];
+  uint64_t k_empty[Rings<kSplit>::kK];
+  uint64_t v_full[Rings<kSplit>::kV];
+  uint64_t v_empty[Rings<kSplit>::kV];
+  uint64_t d_full[Rings<kSplit>::kV];
   uint64_t s_full[2];
-  uint64_t s_empty[2];
+  uint64_t s_free[2];
   uint64_t p_full;
   uint64_t pv_done;
   uint32_t tmem_base;
   uint32_t pad;
-  StepDesc desc[kStages];
+  StepDesc desc[Rings<kSplit>::kV];
 };
 
 template <int kD, bool kSplit>
@@ -70,19 +82,38 @@ struct Layout {
   static constexpr int kCopies = kSplit ? 2 : 1;
   static constexpr int kAtoms = kD / 64;
   static constexpr int kQBytes = kRows * kD * 2;   // one copy
-  static constexpr int kKBytes = kBox * kD * 2;    // one copy of K (or V) per stage
-  static constexpr int kPBytes = kRows * kBox * 2;
+  static constexpr int kKBytes = kBox * kD * 2;    // one copy of one K (or V) tile
   static constexpr int kOffQ = 0;
-  static constexpr int kOffStage = kOffQ + kCopies * kQBytes;
-  static constexpr int kStageBytes = 2 * kCopies * kKBytes;  // K copies then V copies
-  static constexpr int kOffP = kOffStage + kStages * kStageBytes;
-  static constexpr int kOffCtrl = kOffP + kCopies * kPBytes;
-  static constexpr int kSmem = kOffCtrl + (int)sizeof(Ctrl);
-  static constexpr uint32_t kTxStage = 2u * kCopies * kKBytes;
+  static constexpr int kOffK = kOffQ + kCopies * kQBytes;
+  static constexpr int kOffV = kOffK + Rings<kSplit>::kK * kCopies * kKBytes;
+  static constexpr int kOffCtrl = kOffV + Rings<kSplit>::kV * kCopies * kKBytes;
+  static constexpr int kSmem = kOffCtrl + (int)sizeof(Ctrl<kSplit>);
+  static constexpr uint32_t kTxKV = kCopies * kKBytes;
   static constexpr uint32_t kTxQ = kCopies * kQBytes;
 };
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+
+// D[tmem] (+)= A[tmem] * B[smem]: P (bf16, K-major, 2 per 32-bit column) times V.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// One step of the loader's schedule.
+struct StepInfo {
+  int kind;
+  int box, width;
+  unsigned long long mask;
+  int64_t s0;  // chip: first column index (into col_indices)
+  int n;       // chip: keys in this step
+  bool first;  // chip: first 64-key step of a chip (prefix max restarts)
+};
 
 template <int kD, bool kSplit>
 __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
@@ -91,8 +122,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
                            const __grid_constant__ CUtensorMap tm_k2, const __grid_constant__ CUtensorMap tm_v2,
                            const AttnArgs p, int n_ctile, float scale_log2) {
   using L = Layout<kD, kSplit>;
+  using R = Rings<kSplit>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + L::kOffCtrl);
+  Ctrl<kSplit>* ctrl = reinterpret_cast<Ctrl<kSplit>*>(smem + L::kOffCtrl);
   const uint32_t sbase = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5;
@@ -117,13 +149,18 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       __trap();
     }
     mbar_init(&ctrl->q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&ctrl->kv_full[s], 1);
-      mbar_init(&ctrl->kv_empty[s], 1);
+    for (int s = 0; s < R::kK; ++s) {
+      mbar_init(&ctrl->k_full[s], 1);
+      mbar_init(&ctrl->k_empty[s], 1);
+    }
+    for (int s = 0; s < R::kV; ++s) {
+      mbar_init(&ctrl->v_full[s], 1);
+      mbar_init(&ctrl->v_empty[s], 1);
+      mbar_init(&ctrl->d_full[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ctrl->s_full[s], 1);
-      mbar_init(&ctrl->s_empty[s], 128);
+      mbar_init(&ctrl->s_free[s], 1);
     }
     mbar_init(&ctrl->p_full, 128);
     mbar_init(&ctrl->pv_done, 1);
@@ -149,137 +186,233 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       }
     }
     const int64_t row0 = (int64_t)h * n_rows + r_first;
-    int64_t pos[64], endp[64];
-    int cur[64];
-    for (int g = 0; g < G; ++g) {
-      pos[g] = p.tile_offsets[row0 + g];
-      endp[g] = p.tile_offsets[row0 + g + 1];
-      cur[g] = pos[g] < endp[g] ? p.tile_starts[pos[g]] : INT_MAX;
-    }
-    int t = 0;
     const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(p.k_hi) + (int64_t)kvh * S * kD;
     const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(p.v_hi) + (int64_t)kvh * S * kD;
     const __nv_bfloat16* kb2 = kSplit ? reinterpret_cast<const __nv_bfloat16*>(p.k_lo) + (int64_t)kvh * S * kD : nullptr;
     const __nv_bfloat16* vb2 = kSplit ? reinterpret_cast<const __nv_bfloat16*>(p.v_lo) + (int64_t)kvh * S * kD : nullptr;
 
-    // --- tiles: union over the G row blocks, ascending start ---
-    while (true) {
-      int best = INT_MAX;
-      for (int g = 0; g < G; ++g) best = min(best, cur[g]);
-      if (best == INT_MAX) break;
-      unsigned long long mask = 0ull;
-      for (int g = 0; g < G; ++g) {
-        if (cur[g] == best) {
-          mask |= 1ull << g;
-          ++pos[g];
-          cur[g] = pos[g] < endp[g] ? p.tile_starts[pos[g]] : INT_MAX;
-        }
-      }
-      for (int sub = 0; sub * kBox < B; ++sub) {
-        const int st = t % kStages;
-        if (lane == 0) {
-          mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
-          StepDesc& d = ctrl->desc[st];
-          d.kind = kTile;
-          d.box = best + sub * kBox;
-          d.width = min(kBox, B - sub * kBox);
-          d.segmask = mask;
-          uint8_t* kst = smem + L::kOffStage + st * L::kStageBytes;
-          uint8_t* vst = kst + L::kCopies * L::kKBytes;
-          mbar_arrive_expect_tx(&ctrl->kv_full[st], L::kTxStage);
+    // ---- step generator (warp-uniform) ----
+    // Tiles: union over the G row blocks, DESCENDING start (the diagonal tile first,
+    // so the running max is set early and lazy rescales are rare).  Lane l walks the
+    // lists of row blocks l and l + 32 from their ends, holding the next kBuf starts
+    // in registers; one warp max-reduction per union tile.
+    constexpr int kBuf = 8;
+    int cur[2], bn[2];
+    int64_t nxt[2], beg[2];
+    int buf[2][kBuf];
 #pragma unroll
-          for (int a = 0; a < L::kAtoms; ++a) {
-            tma_load_3d(kst + a * (kBox * 128), &tm_k, &ctrl->kv_full[st], a * 64, best + sub * kBox, kvh);
-            tma_load_3d(vst + a * (kBox * 128), &tm_v, &ctrl->kv_full[st], a * 64, best + sub * kBox, kvh);
-            if (kSplit) {
-              tma_load_3d(kst + L::kKBytes + a * (kBox * 128), &tm_k2, &ctrl->kv_full[st], a * 64, best + sub * kBox, kvh);
-              tma_load_3d(vst + L::kKBytes + a * (kBox * 128), &tm_v2, &ctrl->kv_full[st], a * 64, best + sub * kBox, kvh);
-            }
-          }
-        }
-        __syncwarp();
-        ++t;
-      }
+    for (int sl = 0; sl < 2; ++sl) {
+      const int g = lane + 32 * sl;
+      beg[sl] = g < G ? p.tile_offsets[row0 + g] : 0;
+      nxt[sl] = (g < G ? p.tile_offsets[row0 + g + 1] : 0) - 1;  // next index to fetch (descending)
+      bn[sl] = 0;
     }
-    // --- column chips: per row block, chips of B columns, split in 64-key steps ---
-    for (int g = 0; g < G; ++g) {
-      const int64_t cb = p.col_offsets[row0 + g], ce = p.col_offsets[row0 + g + 1];
-      for (int64_t c0 = cb; c0 < ce; c0 += B) {
-        const int64_t chip_end = min(c0 + (int64_t)B, ce);
-        int running = INT_MIN;
-        for (int64_t s0 = c0; s0 < chip_end; s0 += kBox) {
-          const int n = (int)min((int64_t)kBox, chip_end - s0);
-          const int st = t % kStages;
-          if (lane == 0) mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
-          __syncwarp();
-          StepDesc& d = ctrl->desc[st];
-          // prefix max of the keys (two 32-wide warp scans)
-          int key_a = lane < n ? p.col_indices[s0 + lane] : INT_MIN;
-          int key_b = lane + 32 < n ? p.col_indices[s0 + lane + 32] : INT_MIN;
-          int pa = key_a, pb = key_b;
+    auto refill = [&](int sl) {
 #pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            int xa = __shfl_up_sync(0xffffffffu, pa, off);
-            int xb = __shfl_up_sync(0xffffffffu, pb, off);
-            if (lane >= off) { pa = max(pa, xa); pb = max(pb, xb); }
-          }
-          pa = max(pa, running);
-          const int tail_a = __shfl_sync(0xffffffffu, pa, 31);
-          pb = max(pb, tail_a);
-          d.pmax[lane] = pa;
-          d.pmax[lane + 32] = pb;
-          running = __shfl_sync(0xffffffffu, pb, 31);
-          if (lane == 0) {
-            d.kind = kChip;
-            d.box = 0;
-            d.width = n;
-            d.segmask = 1ull << g;
-          }
-          // gather K/V rows (16-byte chunks), writing the SW128 layout by hand
-          uint8_t* kst = smem + L::kOffStage + st * L::kStageBytes;
-          uint8_t* vst = kst + L::kCopies * L::kKBytes;
-          constexpr int kChunksPerRow = kD / 8;
-          for (int idx = lane; idx < kBox * kChunksPerRow; idx += 32) {
-            const int j = idx / kChunksPerRow;
-            const int c16 = idx % kChunksPerRow;
-            const int atom = c16 >> 3, c = c16 & 7;
-            const uint32_t off = atom * (kBox * 128) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4);
-            int4 kv = make_int4(0, 0, 0, 0), vv = make_int4(0, 0, 0, 0);
-            int4 kv2 = make_int4(0, 0, 0, 0), vv2 = make_int4(0, 0, 0, 0);
-            if (j < n) {
-              const int key = p.col_indices[s0 + j];
-              const int64_t e = (int64_t)key * kD + c16 * 8;
-              kv = __ldg(reinterpret_cast<const int4*>(kb + e));
-              vv = __ldg(reinterpret_cast<const int4*>(vb + e));
-              if (kSplit) {
-                kv2 = __ldg(reinterpret_cast<const int4*>(kb2 + e));
-                vv2 = __ldg(reinterpret_cast<const int4*>(vb2 + e));
+      for (int u = 0; u < kBuf; ++u) buf[sl][u] = (nxt[sl] - u >= beg[sl]) ? p.tile_starts[nxt[sl] - u] : INT_MIN;
+      const int64_t avail = nxt[sl] - beg[sl] + 1;
+      bn[sl] = (int)(avail < kBuf ? avail : kBuf);
+      nxt[sl] -= bn[sl];
+    };
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      if (nxt[sl] >= beg[sl]) refill(sl);
+      cur[sl] = bn[sl] > 0 ? buf[sl][0] : INT_MIN;
+    }
+    int phase = 0;           // 0: tiles, 1: chips, 2: done
+    int tile_best = 0, tile_sub = 0, n_sub = (B + kBox - 1) / kBox;
+    unsigned long long tile_mask = 0ull;
+    bool tile_open = false;
+    int cg = 0;              // chips: row block
+    int64_t c0 = 0, cend = 0, s0 = 0, chip_end = 0;
+    bool chip_open = false, chip_first = false;
+    if (G > 0) {
+      c0 = p.col_offsets[row0];
+      cend = p.col_offsets[row0 + 1];
+    }
+    auto next_step = [&](StepInfo& st) {
+      if (phase == 0) {
+        if (!tile_open) {
+          const int best = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
+          if (best == INT_MIN) {
+            phase = 1;
+          } else {
+            const bool hit0 = cur[0] == best, hit1 = cur[1] == best;
+            tile_mask = (unsigned long long)__ballot_sync(0xffffffffu, hit0) |
+                        ((unsigned long long)__ballot_sync(0xffffffffu, hit1) << 32);
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              if (sl == 0 ? hit0 : hit1) {
+#pragma unroll
+                for (int u = 0; u + 1 < kBuf; ++u) buf[sl][u] = buf[sl][u + 1];
+                if (--bn[sl] == 0 && nxt[sl] >= beg[sl]) refill(sl);
+                cur[sl] = bn[sl] > 0 ? buf[sl][0] : INT_MIN;
               }
             }
-            *reinterpret_cast<int4*>(kst + off) = kv;
-            *reinterpret_cast<int4*>(vst + off) = vv;
-            if (kSplit) {
-              *reinterpret_cast<int4*>(kst + L::kKBytes + off) = kv2;
-              *reinterpret_cast<int4*>(vst + L::kKBytes + off) = vv2;
-            }
+            tile_best = best;
+            tile_sub = 0;
+            tile_open = true;
           }
-          fence_proxy_async_smem();
-          __threadfence_block();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctrl->kv_full[st]);
-          ++t;
+        }
+        if (phase == 0) {
+          st.kind = kTile;
+          st.box = tile_best + tile_sub * kBox;
+          st.width = min(kBox, B - tile_sub * kBox);
+          st.mask = tile_mask;
+          if (++tile_sub == n_sub) tile_open = false;
+          return;
         }
       }
-    }
-    // --- end marker ---
-    {
-      const int st = t % kStages;
-      if (lane == 0) {
-        mbar_wait(&ctrl->kv_empty[st], ((t / kStages) & 1) ^ 1);
-        ctrl->desc[st].kind = kEnd;
-        mbar_arrive(&ctrl->kv_full[st]);
+      if (phase == 1) {
+        // chips: per row block, chips of B columns, each split in 64-key steps
+        while (!chip_open) {
+          if (c0 < cend) {
+            chip_end = min(c0 + (int64_t)B, cend);
+            s0 = c0;
+            chip_open = true;
+            chip_first = true;
+          } else if (++cg < G) {
+            c0 = p.col_offsets[row0 + cg];
+            cend = p.col_offsets[row0 + cg + 1];
+          } else {
+            phase = 2;
+            break;
+          }
+        }
+        if (phase == 1) {
+          st.kind = kChip;
+          st.s0 = s0;
+          st.n = (int)min((int64_t)kBox, chip_end - s0);
+          st.mask = 1ull << cg;
+          st.first = chip_first;
+          chip_first = false;
+          s0 += kBox;
+          if (s0 >= chip_end) {
+            chip_open = false;
+            c0 = chip_end;
+          }
+          return;
+        }
+      }
+      st.kind = kEnd;
+    };
+
+    // gather 64 rows (16-byte chunks) of K or V by column index into a SW128 tile
+    auto gather = [&](uint8_t* dst, const __nv_bfloat16* src, const __nv_bfloat16* src2, const StepInfo& st) {
+      constexpr int kChunksPerRow = kD / 8;
+      for (int idx = lane; idx < kBox * kChunksPerRow; idx += 32) {
+        const int j = idx / kChunksPerRow;
+        const int c16 = idx % kChunksPerRow;
+        const int atom = c16 >> 3, c = c16 & 7;
+        const uint32_t off = atom * (kBox * 128) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4);
+        int4 x = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
+        if (j < st.n) {
+          const int key = p.col_indices[st.s0 + j];
+          const int64_t e = (int64_t)key * kD + c16 * 8;
+          x = __ldg(reinterpret_cast<const int4*>(src + e));
+          if (kSplit) x2 = __ldg(reinterpret_cast<const int4*>(src2 + e));
+        }
+        *reinterpret_cast<int4*>(dst + off) = x;
+        if (kSplit) *reinterpret_cast<int4*>(dst + L::kKBytes + off) = x2;
+      }
+      fence_proxy_async_smem();
+      __threadfence_block();
+      __syncwarp();
+    };
+
+    auto issue_k = [&](int t, const StepInfo& st) {
+      const int sk = t % R::kK;
+      uint8_t* kst = smem + L::kOffK + sk * (L::kCopies * L::kKBytes);
+      if (lane == 0) mbar_wait(&ctrl->k_empty[sk], ((t / R::kK) & 1) ^ 1);
+      __syncwarp();
+      if (st.kind == kTile) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&ctrl->k_full[sk], L::kTxKV);
+#pragma unroll
+          for (int a = 0; a < L::kAtoms; ++a) {
+            tma_load_3d(kst + a * (kBox * 128), &tm_k, &ctrl->k_full[sk], a * 64, st.box, kvh);
+            if (kSplit) tma_load_3d(kst + L::kKBytes + a * (kBox * 128), &tm_k2, &ctrl->k_full[sk], a * 64, st.box, kvh);
+          }
+        }
+      } else {
+        gather(kst, kb, kb2, st);
+        if (lane == 0) mbar_arrive(&ctrl->k_full[sk]);
       }
       __syncwarp();
+    };
+
+    int running = INT_MIN;  // chip prefix max, carried across a chip's 64-key steps
+    auto issue_v = [&](int t, const StepInfo& st) {
+      const int sv = t % R::kV;
+      uint8_t* vst = smem + L::kOffV + sv * (L::kCopies * L::kKBytes);
+      if (lane == 0) mbar_wait(&ctrl->v_empty[sv], ((t / R::kV) & 1) ^ 1);
+      __syncwarp();
+      StepDesc& d = ctrl->desc[sv];
+      if (st.kind == kChip) {
+        if (st.first) running = INT_MIN;
+        // prefix max of the keys (two 32-wide warp scans)
+        int key_a = lane < st.n ? p.col_indices[st.s0 + lane] : INT_MIN;
+        int key_b = lane + 32 < st.n ? p.col_indices[st.s0 + lane + 32] : INT_MIN;
+        int pa = key_a, pb = key_b;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          int xa = __shfl_up_sync(0xffffffffu, pa, off);
+          int xb = __shfl_up_sync(0xffffffffu, pb, off);
+          if (lane >= off) { pa = max(pa, xa); pb = max(pb, xb); }
+        }
+        pa = max(pa, running);
+        const int tail_a = __shfl_sync(0xffffffffu, pa, 31);
+        pb = max(pb, tail_a);
+        d.pmax[lane] = pa;
+        d.pmax[lane + 32] = pb;
+        running = __shfl_sync(0xffffffffu, pb, 31);
+        gather(vst, vb, vb2, st);
+        if (lane == 0) {
+          d.kind = kChip;
+          d.box = 0;
+          d.width = st.n;
+          d.segmask = st.mask;
+          mbar_arrive(&ctrl->d_full[sv]);
+          mbar_arrive(&ctrl->v_full[sv]);
+        }
+      } else if (lane == 0) {
+        d.kind = st.kind;
+        d.box = st.box;
+        d.width = st.width;
+        d.segmask = st.mask;
+        mbar_arrive(&ctrl->d_full[sv]);
+        if (st.kind == kTile) {
+          mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
+#pragma unroll
+          for (int a = 0; a < L::kAtoms; ++a) {
+            tma_load_3d(vst + a * (kBox * 128), &tm_v, &ctrl->v_full[sv], a * 64, st.box, kvh);
+            if (kSplit) tma_load_3d(vst + L::kKBytes + a * (kBox * 128), &tm_v2, &ctrl->v_full[sv], a * 64, st.box, kvh);
+          }
+        }
+      }
+      __syncwarp();
+    };
+
+    // schedule: K of step t+1 is issued before V of step t
+    StepInfo pend;
+    bool have_pend = false;
+    int t = 0;
+    while (true) {
+      StepInfo st;
+      next_step(st);
+      if (st.kind != kEnd) issue_k(have_pend ? t + 1 : t, st);
+      if (have_pend) {
+        issue_v(t, pend);
+        ++t;
+      }
+      if (st.kind == kEnd) break;
+      pend = st;
+      have_pend = true;
+    }
+    {
+      StepInfo end_st;
+      end_st.kind = kEnd;
+      issue_v(t, end_st);  // end marker through the descriptor ring
     }
   } else if (warp == 1) {
     // =============================== MMA issuer ================================
@@ -287,42 +420,44 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       constexpr uint32_t idesc_qk = umma_idesc_bf16(128, kBox, 0, 0);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(128, kD, 0, 1);
       const uint32_t q_addr = sbase + L::kOffQ;
-      const uint32_t p_addr = sbase + L::kOffP;
       const uint32_t tO = tmem + 128;
       mbar_wait(&ctrl->q_full, 0);
       tc_fence_after();
 
       auto issue_pv = [&](int u) {
+        const int sv = u % R::kV;
         mbar_wait(&ctrl->p_full, u & 1);
+        mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
         tc_fence_after();
-        const int st = u % kStages;
-        const uint32_t v_addr = sbase + L::kOffStage + st * L::kStageBytes + L::kCopies * L::kKBytes;
+        const uint32_t v_addr = sbase + L::kOffV + sv * (L::kCopies * L::kKBytes);
+        const uint32_t tP = tmem + (u & 1) * kBox;  // P(u) overwrote S(u): hi in cols 0..31, lo in 32..63
 #pragma unroll
         for (int k = 0; k < kBox / 16; ++k) {
-          const uint64_t a_hi = umma_desc_sw128(p_addr + k * 32, 0, 1024);
           const uint64_t b_hi = umma_desc_sw128(v_addr + k * 2048, kBox * 128, 1024);
-          mma_bf16_ss(tO, a_hi, b_hi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
+          mma_bf16_ts(tO, tP + k * 8, b_hi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
           if (kSplit) {
-            const uint64_t a_lo = umma_desc_sw128(p_addr + L::kPBytes + k * 32, 0, 1024);
             const uint64_t b_lo = umma_desc_sw128(v_addr + L::kKBytes + k * 2048, kBox * 128, 1024);
-            mma_bf16_ss(tO, a_hi, b_lo, idesc_pv, 1u);
-            mma_bf16_ss(tO, a_lo, b_hi, idesc_pv, 1u);
+            mma_bf16_ts(tO, tP + k * 8, b_lo, idesc_pv, 1u);
+            mma_bf16_ts(tO, tP + 32 + k * 8, b_hi, idesc_pv, 1u);
           }
         }
         mma_commit(&ctrl->pv_done);
-        mma_commit(&ctrl->kv_empty[st]);
+        mma_commit(&ctrl->v_empty[sv]);
+        mma_commit(&ctrl->s_free[u & 1]);
       };
 
       int t = 0;
       for (;; ++t) {
-        const int st = t % kStages;
-        mbar_wait(&ctrl->kv_full[st], (t / kStages) & 1);
-        const int kind = *reinterpret_cast<volatile int*>(&ctrl->desc[st].kind);
+        const int sv = t % R::kV;
+        mbar_wait(&ctrl->d_full[sv], (t / R::kV) & 1);
+        const int kind = *reinterpret_cast<volatile int*>(&ctrl->desc[sv].kind);
         if (kind == kEnd) break;
+        const int sk = t % R::kK;
         const int sb = t & 1;
-        mbar_wait(&ctrl->s_empty[sb], ((t >> 1) & 1) ^ 1);
+        mbar_wait(&ctrl->k_full[sk], (t / R::kK) & 1);
+        mbar_wait(&ctrl->s_free[sb], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k_addr = sbase + L::kOffStage + st * L::kStageBytes;
+        const uint32_t k_addr = sbase + L::kOffK + sk * (L::kCopies * L::kKBytes);
         const uint32_t tS = tmem + sb * kBox;
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
@@ -339,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
           }
         }
         mma_commit(&ctrl->s_full[sb]);
+        mma_commit(&ctrl->k_empty[sk]);
         if (t > 0) issue_pv(t - 1);
       }
       if (t > 0) issue_pv(t - 1);
@@ -351,14 +487,12 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     const int q = R0 + row;
     const int seg = (q < S) ? (q / B - r_first) : -1;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t p_row = sbase + L::kOffP + (row >> 3) * 1024 + (row & 7) * 128;
-    const int sw = row & 7;
     float m_run = -INFINITY, l_run = 0.f;
     int t = 0;
     for (;; ++t) {
-      const int st = t % kStages;
-      mbar_wait(&ctrl->kv_full[st], (t / kStages) & 1);
-      const StepDesc& d = ctrl->desc[st];
+      const int sv = t % R::kV;
+      mbar_wait(&ctrl->d_full[sv], (t / R::kV) & 1);
+      const StepDesc& d = ctrl->desc[sv];
       const int kind = d.kind;
       if (kind == kEnd) break;
       const int sb = t & 1;
@@ -367,8 +501,6 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       uint32_t x[kBox];
       tmem_ld32x32b_x64(tmem + lane_off + sb * kBox, x);
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&ctrl->s_empty[sb]);
 
       // valid key slots for this row: a contiguous range [lo, hi)
       int lo = 0, hi = 0;
@@ -444,31 +576,28 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       const float sum = sa + sb2;
       l_run = l_run * alpha + sum;
 
+      // PV(t-1) retired (issued right after QK(t), so normally long done): waited every step
+      // so the parity of pv_done never aliases; the O rescale needs it.
       if (t > 0) {
         mbar_wait(&ctrl->pv_done, (t - 1) & 1);
         tc_fence_after();
-        // tcgen05.ld/st are warp-collective (.sync.aligned): decide per warp.
-        if (__any_sync(0xffffffffu, rescale)) {
+      }
+      // tcgen05.ld/st are warp-collective: decide per warp
+      if (t > 0 && __any_sync(0xffffffffu, rescale)) {
 #pragma unroll
-          for (int c = 0; c < kD; c += 32) {
-            uint32_t o[32];
-            tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
-            tmem_wait_ld();
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t o[32];
+          tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-            tmem_st32x32b_x32(tmem + lane_off + 128 + c, o);
-          }
-          tmem_wait_st();
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
+          tmem_st32x32b_x32(tmem + lane_off + 128 + c, o);
         }
       }
-      // P row -> SW128 K-major smem (chunk c of 8 keys lands at chunk c ^ (row & 7))
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        st_shared_v4(p_row + ((c ^ sw) << 4), ph[4 * c], ph[4 * c + 1], ph[4 * c + 2], ph[4 * c + 3]);
-        if (kSplit)
-          st_shared_v4(p_row + L::kPBytes + ((c ^ sw) << 4), pl[4 * c], pl[4 * c + 1], pl[4 * c + 2], pl[4 * c + 3]);
-      }
-      fence_proxy_async_smem();
+      // P(t) -> TMEM over S(t): bf16 pairs, K-major (PV reads A from TMEM)
+      tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
+      if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full);
     }

@@ -43,11 +43,10 @@ constexpr int kThreads = 192;
 enum : int { kTile = 0, kChip = 1, kEnd = 2 };
 
 struct StepDesc {
-  int kind;
-  int box;     // tile: first key of the loaded box
-  int width;   // tile: valid keys in the box ([box, box+width)); chip: number of keys
-  int pad;
   unsigned long long segmask;
+  int box;      // tile: first key of the loaded box
+  short kind;
+  short width;  // tile: valid keys in the box ([box, box+width)); chip: number of keys
   int pmax[kBox];  // chip: running max of the chip's keys (prefix rule)
 };
 
@@ -58,6 +57,7 @@ template <bool kSplit>
 struct Rings {
   static constexpr int kK = kSplit ? 2 : 3;
   static constexpr int kV = 2;
+  static constexpr int kD = 3;  // step descriptors: written with K (one step ahead), freed by the softmax
 };
 
 template <bool kSplit>
@@ -67,15 +67,18 @@ struct Ctrl {
   uint64_t k_empty[Rings<kSplit>::kK];
   uint64_t v_full[Rings<kSplit>::kV];
   uint64_t v_empty[Rings<kSplit>::kV];
-  uint64_t d_full[Rings<kSplit>::kV];
+  uint64_t d_full[Rings<kSplit>::kD];
+  uint64_t d_empty[Rings<kSplit>::kD];
   uint64_t s_full[2];
   uint64_t s_free[2];
   uint64_t p_full;
   uint64_t pv_done;
   uint32_t tmem_base;
   uint32_t pad;
-  StepDesc desc[Rings<kSplit>::kV];
+  StepDesc desc[Rings<kSplit>::kD];
 };
+// two CTAs per SM need kSmem <= 115712 B (228 KB minus 1 KB reserved per CTA)
+static_assert(sizeof(Ctrl<false>) <= 1024, "control block too large for two CTAs per SM");
 
 template <int kD, bool kSplit>
 struct Layout {
@@ -156,7 +159,10 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     for (int s = 0; s < R::kV; ++s) {
       mbar_init(&ctrl->v_full[s], 1);
       mbar_init(&ctrl->v_empty[s], 1);
+    }
+    for (int s = 0; s < R::kD; ++s) {
       mbar_init(&ctrl->d_full[s], 1);
+      mbar_init(&ctrl->d_empty[s], 4);  // one arrival per softmax warp
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ctrl->s_full[s], 1);
@@ -320,6 +326,42 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       __syncwarp();
     };
 
+    int running = INT_MIN;  // chip prefix max, carried across a chip's 64-key steps
+    // descriptor of step t (kind, box/width, segment mask, chip prefix max), ring of R::kD
+    auto write_desc = [&](int t, const StepInfo& st) {
+      const int sd = t % R::kD;
+      if (lane == 0) mbar_wait(&ctrl->d_empty[sd], ((t / R::kD) & 1) ^ 1);
+      __syncwarp();
+      StepDesc& d = ctrl->desc[sd];
+      if (st.kind == kChip) {
+        if (st.first) running = INT_MIN;
+        // prefix max of the keys (two 32-wide warp scans)
+        int key_a = lane < st.n ? p.col_indices[st.s0 + lane] : INT_MIN;
+        int key_b = lane + 32 < st.n ? p.col_indices[st.s0 + lane + 32] : INT_MIN;
+        int pa = key_a, pb = key_b;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          int xa = __shfl_up_sync(0xffffffffu, pa, off);
+          int xb = __shfl_up_sync(0xffffffffu, pb, off);
+          if (lane >= off) { pa = max(pa, xa); pb = max(pb, xb); }
+        }
+        pa = max(pa, running);
+        const int tail_a = __shfl_sync(0xffffffffu, pa, 31);
+        pb = max(pb, tail_a);
+        d.pmax[lane] = pa;
+        d.pmax[lane + 32] = pb;
+        running = __shfl_sync(0xffffffffu, pb, 31);
+      }
+      if (lane == 0) {
+        d.kind = (short)st.kind;
+        d.box = st.kind == kChip ? 0 : st.box;
+        d.width = (short)(st.kind == kChip ? st.n : st.width);
+        d.segmask = st.mask;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_full[sd]);
+    };
+
     auto issue_k = [&](int t, const StepInfo& st) {
       const int sk = t % R::kK;
       uint8_t* kst = smem + L::kOffK + sk * (L::kCopies * L::kKBytes);
@@ -339,61 +381,29 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         if (lane == 0) mbar_arrive(&ctrl->k_full[sk]);
       }
       __syncwarp();
+      write_desc(t, st);
     };
 
-    int running = INT_MIN;  // chip prefix max, carried across a chip's 64-key steps
     auto issue_v = [&](int t, const StepInfo& st) {
       const int sv = t % R::kV;
       uint8_t* vst = smem + L::kOffV + sv * (L::kCopies * L::kKBytes);
       if (lane == 0) mbar_wait(&ctrl->v_empty[sv], ((t / R::kV) & 1) ^ 1);
       __syncwarp();
-      StepDesc& d = ctrl->desc[sv];
       if (st.kind == kChip) {
-        if (st.first) running = INT_MIN;
-        // prefix max of the keys (two 32-wide warp scans)
-        int key_a = lane < st.n ? p.col_indices[st.s0 + lane] : INT_MIN;
-        int key_b = lane + 32 < st.n ? p.col_indices[st.s0 + lane + 32] : INT_MIN;
-        int pa = key_a, pb = key_b;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          int xa = __shfl_up_sync(0xffffffffu, pa, off);
-          int xb = __shfl_up_sync(0xffffffffu, pb, off);
-          if (lane >= off) { pa = max(pa, xa); pb = max(pb, xb); }
-        }
-        pa = max(pa, running);
-        const int tail_a = __shfl_sync(0xffffffffu, pa, 31);
-        pb = max(pb, tail_a);
-        d.pmax[lane] = pa;
-        d.pmax[lane + 32] = pb;
-        running = __shfl_sync(0xffffffffu, pb, 31);
         gather(vst, vb, vb2, st);
-        if (lane == 0) {
-          d.kind = kChip;
-          d.box = 0;
-          d.width = st.n;
-          d.segmask = st.mask;
-          mbar_arrive(&ctrl->d_full[sv]);
-          mbar_arrive(&ctrl->v_full[sv]);
-        }
+        if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
       } else if (lane == 0) {
-        d.kind = st.kind;
-        d.box = st.box;
-        d.width = st.width;
-        d.segmask = st.mask;
-        mbar_arrive(&ctrl->d_full[sv]);
-        if (st.kind == kTile) {
-          mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
+        mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
 #pragma unroll
-          for (int a = 0; a < L::kAtoms; ++a) {
-            tma_load_3d(vst + a * (kBox * 128), &tm_v, &ctrl->v_full[sv], a * 64, st.box, kvh);
-            if (kSplit) tma_load_3d(vst + L::kKBytes + a * (kBox * 128), &tm_v2, &ctrl->v_full[sv], a * 64, st.box, kvh);
-          }
+        for (int a = 0; a < L::kAtoms; ++a) {
+          tma_load_3d(vst + a * (kBox * 128), &tm_v, &ctrl->v_full[sv], a * 64, st.box, kvh);
+          if (kSplit) tma_load_3d(vst + L::kKBytes + a * (kBox * 128), &tm_v2, &ctrl->v_full[sv], a * 64, st.box, kvh);
         }
       }
       __syncwarp();
     };
 
-    // schedule: K of step t+1 is issued before V of step t
+    // schedule: K (and the descriptor) of step t+1 is issued before V of step t
     StepInfo pend;
     bool have_pend = false;
     int t = 0;
@@ -401,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       StepInfo st;
       next_step(st);
       if (st.kind != kEnd) issue_k(have_pend ? t + 1 : t, st);
+      else write_desc(have_pend ? t + 1 : t, st);  // end marker through the descriptor ring
       if (have_pend) {
         issue_v(t, pend);
         ++t;
@@ -408,11 +419,6 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       if (st.kind == kEnd) break;
       pend = st;
       have_pend = true;
-    }
-    {
-      StepInfo end_st;
-      end_st.kind = kEnd;
-      issue_v(t, end_st);  // end marker through the descriptor ring
     }
   } else if (warp == 1) {
     // =============================== MMA issuer ================================
@@ -448,9 +454,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
 
       int t = 0;
       for (;; ++t) {
-        const int sv = t % R::kV;
-        mbar_wait(&ctrl->d_full[sv], (t / R::kV) & 1);
-        const int kind = *reinterpret_cast<volatile int*>(&ctrl->desc[sv].kind);
+        const int sd = t % R::kD;
+        mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
+        const int kind = *reinterpret_cast<volatile short*>(&ctrl->desc[sd].kind);
         if (kind == kEnd) break;
         const int sk = t % R::kK;
         const int sb = t & 1;
@@ -490,9 +496,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     float m_run = -INFINITY, l_run = 0.f;
     int t = 0;
     for (;; ++t) {
-      const int sv = t % R::kV;
-      mbar_wait(&ctrl->d_full[sv], (t / R::kV) & 1);
-      const StepDesc& d = ctrl->desc[sv];
+      const int sd = t % R::kD;
+      mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
+      const StepDesc& d = ctrl->desc[sd];
       const int kind = d.kind;
       if (kind == kEnd) break;
       const int sb = t & 1;
@@ -517,6 +523,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
           hi = a;
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
       // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
       if (!(lo == 0 && hi == kBox)) {
 #pragma unroll

@@ -73,6 +73,7 @@ struct Ctrl {
   uint64_t s_free[2];
   uint64_t p_full;
   uint64_t pv_done;
+  uint64_t o_ready;  // all PVs retired (committed once after the last one)
   uint32_t tmem_base;
   uint32_t pad;
   StepDesc desc[Rings<kSplit>::kD];
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     }
     mbar_init(&ctrl->p_full, 128);
     mbar_init(&ctrl->pv_done, 1);
+    mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&ctrl->tmem_base, 256);
@@ -484,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         if (t > 0) issue_pv(t - 1);
       }
       if (t > 0) issue_pv(t - 1);
+      mma_commit(&ctrl->o_ready);
     }
     __syncwarp();
   } else {
@@ -584,14 +587,12 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       const float sum = sa + sb2;
       l_run = l_run * alpha + sum;
 
-      // PV(t-1) retired (issued right after QK(t), so normally long done): waited every step
-      // so the parity of pv_done never aliases; the O rescale needs it.
-      if (t > 0) {
+      // O rescale needs PV(t-1) retired.  S(t) being ready implies PV(t-2) retired (QK(t)
+      // waited s_free), so pv_done has completed t-1 or t phases: the parity wait for
+      // phase t-1 cannot alias.  tcgen05.ld/st are warp-collective: decide per warp.
+      if (t > 0 && __any_sync(0xffffffffu, rescale)) {
         mbar_wait(&ctrl->pv_done, (t - 1) & 1);
         tc_fence_after();
-      }
-      // tcgen05.ld/st are warp-collective: decide per warp
-      if (t > 0 && __any_sync(0xffffffffu, rescale)) {
 #pragma unroll
         for (int c = 0; c < kD; c += 32) {
           uint32_t o[32];
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     }
     // ---- epilogue: O / l -> global ----
     if (t > 0) {
-      mbar_wait(&ctrl->pv_done, (t - 1) & 1);
+      mbar_wait(&ctrl->o_ready, 0);
       tc_fence_after();
     }
     {

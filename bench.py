@@ -7,11 +7,12 @@ configs/llama3_8b_1m_c2.json), G-local synthetic bf16 inputs (SURVEY.md
 8(d)).  One step = estimation + index compaction + sparse attention for all
 32 layers (1024 heads), inputs resident in HBM (48 GB > L2, no flush needed).
 
-    python bench.py [--gpus N --steps K --warmup W] [--config c2|c3|c5] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config c2|c3|c4|c5] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): heads are sharded by kv group (no
-data-path collective; strong scaling of the fixed C2 job), time = max over
-ranks.  ``--impl reference`` times the reference's CPU path on the host cores.
+Multi-GPU (torchrun, one rank per GPU): q-heads are sharded over ranks
+(paper_2407_02490_b200/sharding.py: whole kv groups when N divides the kv
+heads; no data-path collective; strong scaling of the fixed job), time = max
+over ranks.  ``--impl reference`` times the reference's CPU path on the host cores.
 """
 
 from __future__ import annotations
@@ -37,6 +38,8 @@ CONFIGS = {
                patterns="configs/llama3_8b_1m_c2.json", inputs="G-local"),
     "c3": dict(workload="c3_llama3_8b_1m_attention_1L_1m_vs", seq_len=1048576, hq=32, hkv=8, layers=1,
                patterns="VS(1000,6096) all heads", inputs="G-local"),
+    "c4": dict(workload="c4_yi_200k_attention_1L_256k_bs", seq_len=262144, hq=56, hkv=8, layers=1,
+               patterns="BS(100) all heads", inputs="G-iid"),
     "c5": dict(workload="c5_qwen2_7b_attention_1L_512k_ashape", seq_len=524288, hq=28, hkv=4, layers=1,
                patterns="AShape(128,4096) all heads", inputs="G-iid"),
 }
@@ -57,8 +60,12 @@ def layer_configs(cfg):
 
     if cfg["patterns"].endswith(".json"):
         return load_layer_configs(os.path.join(REPO, cfg["patterns"]))
+    from paper_2407_02490_b200.patterns import BlockSparse
+
     if cfg["patterns"].startswith("VS"):
         return [[VerticalSlash(1000, 6096)] * cfg["hq"] for _ in range(cfg["layers"])]
+    if cfg["patterns"].startswith("BS"):
+        return [[BlockSparse(100)] * cfg["hq"] for _ in range(cfg["layers"])]
     return [[AShape(128, 4096)] * cfg["hq"] for _ in range(cfg["layers"])]
 
 
@@ -190,12 +197,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     S, HQ, HKV, L, D, B = cfg["seq_len"], cfg["hq"], cfg["hkv"], cfg["layers"], 128, 64
-    if HKV % world:
-        raise SystemExit(f"--gpus {world} must divide the {HKV} kv heads")
-    kv_per = HKV // world
-    q_per_kv = HQ // HKV
-    hq_loc = kv_per * q_per_kv
-    q0 = rank * hq_loc
+    from paper_2407_02490_b200.sharding import max_over_ranks, shard_heads
+
+    shard = shard_heads(HQ, HKV, world, rank)
+    hq_loc = shard.n_q
+    q0 = shard.q_begin
     all_cfgs = layer_configs(cfg)[:L]
     cfgs = [row[q0:q0 + hq_loc] for row in all_cfgs]
     gen = g_local_qkv if cfg["inputs"] == "G-local" else g_iid_qkv
@@ -205,8 +211,8 @@ def main():
     for layer in range(L):
         q, k, v = gen(HQ, HKV, S, D, seed=1000 * layer, device=dev)
         Q.append(q[q0:q0 + hq_loc].contiguous())
-        K.append(k[rank * kv_per:(rank + 1) * kv_per].contiguous())
-        V.append(v[rank * kv_per:(rank + 1) * kv_per].contiguous())
+        K.append(k[shard.kv_begin:shard.kv_end].contiguous())
+        V.append(v[shard.kv_begin:shard.kv_end].contiguous())
         del q, k, v
     out = torch.empty((hq_loc, S, D), dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream()
@@ -265,11 +271,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    elapsed = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
+    elapsed = max_over_ranks(t0.elapsed_time(t1), device=dev)
     ms_per_step = elapsed / args.steps
     attn_ms = [a.elapsed_time(b) for a, b in attn_events]
     attn_avg = sum(attn_ms) / len(attn_ms)
@@ -301,10 +303,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, P, torch, Q, K, V, cfgs, B, L, stream)
-        if world > 1:
-            tt = torch.tensor([e2e["value"]], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = round(float(tt.item()), 3)
+        e2e["value"] = round(max_over_ranks(e2e["value"], device=dev), 3)
 
     # ---- dense FlashAttention-class baseline (torch SDPA, bf16, causal, GQA), one layer ----
     dense = None
@@ -328,7 +327,8 @@ def main():
                        "pattern_heads_this_rank": pattern_counts, "inputs": cfg["inputs"] + " (SURVEY.md 8d)",
                        "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush" % (
                            sum(t.numel() * 2 for t in Q + K + V) / 1e9),
-                       "parallelism": f"heads sharded by kv group over {world} GPU(s), no collective",
+                       "parallelism": f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
+                                      f"divides {HKV}), no data-path collective",
                        "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
                        "union_steps": union_tot},
             "roofline": roofline,

@@ -156,3 +156,44 @@ def test_argtopk_ties(P):
     assert P.argtopk([3.0, 1.0], 10).tolist() == [0, 1]
     with pytest.raises(ValueError):
         P.argtopk([1.0], 0)
+
+
+@pytest.mark.parametrize("hq,hkv,ids", [(14, 2, None), (7, 1, [6, 0, 3, 5]), (12, 4, [11, 2, 7]), (8, 8, [1, 6])])
+def test_vs_fast_gqa_grouping_matches_exact(P, hq, hkv, ids):
+    """Groups of up to 4 q-heads per kv head (7 q-heads per kv head -> 2 groups), head
+    subsets in arbitrary order: the production path equals the fp64 path head by head."""
+    from benchmarks.workloads import g_local_qkv
+
+    from paper_2407_02490_b200.estimator import vs_estimate_async
+
+    s = 4096 + 64 * 3 + 17
+    q, k, _ = g_local_qkv(hq, hkv, s, 128, seed=hq + hkv, device="cuda")
+    cfg = P.VerticalSlash(300, 900, 64)
+    head_ids = None if ids is None else torch.tensor(ids, dtype=torch.int32, device="cuda")
+    vf, sf, _, _, _ = vs_estimate_async(q, k, cfg, head_ids, mode="fast")
+    ve, se, _, _, _ = vs_estimate_async(q, k, cfg, head_ids, mode="exact")
+    assert torch.equal(vf, ve) and torch.equal(sf, se)
+    # and against the CPU oracle for two of the heads
+    qn, kn = q.float().cpu().numpy(), k.float().cpu().numpy()
+    for i, h in list(enumerate(ids if ids is not None else range(hq)))[:2]:
+        wv, ws = port.estimate_vertical_slash(qn[h], kn[h // (hq // hkv)], 300, 900, 64)
+        np.testing.assert_array_equal(vf[i].cpu().numpy(), wv)
+        np.testing.assert_array_equal(sf[i].cpu().numpy(), ws)
+
+
+def test_vs_ties_resolved_by_lowest_index(P):
+    """Repeated identical keys make exactly tied vertical scores: the reference's
+    stable order (ties to the lower index, estimator.py:66) must hold on both paths."""
+    s, d = 2048, 64
+    rng = np.random.Generator(np.random.PCG64(11))
+    q = bf16_round(rng.standard_normal((s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((s, d)).astype(np.float32))
+    k[100:1700:4] = k[90]  # 400 identical columns (tied vertical sums)
+    cfg = P.VerticalSlash(150, 200, 64)
+    wv, ws = port.estimate_vertical_slash(q, k, 150, 200, 64)
+    tq = torch.from_numpy(q).cuda().to(torch.bfloat16)[None]
+    tk = torch.from_numpy(k).cuda().to(torch.bfloat16)[None]
+    for mode in ("fast", "exact"):
+        vert, sl = P.estimate_vertical_slash_gpu(tq, tk, cfg, mode=mode)
+        np.testing.assert_array_equal(vert[0].cpu().numpy(), wv, err_msg=mode)
+        np.testing.assert_array_equal(sl[0].cpu().numpy(), ws, err_msg=mode)

@@ -696,7 +696,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
     attr_done = true;
   }
   const int n_ctile = (a.S + kRows - 1) / kRows;
-  const long long grid = (long long)n_ctile * a.Hq;
+  const long long grid = a.work_order != nullptr ? (long long)a.n_work : (long long)n_ctile * a.Hq;
   if (grid == 0) return 0;
   if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
   const float scale_log2 = a.scale * 1.4426950408889634f;
@@ -710,6 +710,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream) {
   if (a.B < 2) return set_error(2, "block_size must be >= 2 for the sm_100a kernel (got %d)", a.B);
   if (a.Hkv <= 0 || a.Hq % a.Hkv != 0) return set_error(2, "n_q_heads must be a multiple of n_kv_heads");
+  if (attn2_supported(a)) return launch_sparse_attn2(a, stream);
   if (a.kD == 128) return a.split ? launch_impl<128, true>(a, stream) : launch_impl<128, false>(a, stream);
   if (a.kD == 64) return a.split ? launch_impl<64, true>(a, stream) : launch_impl<64, false>(a, stream);
   return set_error(2, "padded head_dim must be 64 or 128 (got %d)", a.kD);

@@ -146,6 +146,7 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
   a.kD = kD;
   a.split = split;
   a.work_order = nullptr;
+  a.n_work = 0;
   const size_t need = spf_sparse_flash_workspace_size(dtype, n_q_heads, n_kv_heads, seq_len, head_dim);
   if (need == 0) {
     a.q_hi = q;

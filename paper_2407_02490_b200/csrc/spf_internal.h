@@ -31,10 +31,14 @@ struct AttnArgs {
   bool out_f32;
   int kD;
   bool split;
-  const int32_t* work_order;  // optional: CTA -> work-item permutation (nullptr = heavy rows first)
+  const int32_t* work_order;  // optional: CTA -> work-item list (nullptr = all items, heavy rows first)
+  int n_work;                 // number of entries in work_order
 };
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
+// Two-tile (256-row) bf16 kernel, attn_fwd2.cu.
+bool attn2_supported(const AttnArgs& a);
+int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream);
 
 // fp64 Vertical-Slash estimation (estimate_vs_exact.cu): all heads (gate == nullptr) or the
 // flagged ones; tile_max / row_mc (from the tensor-core pass, last_q 64) enable exact tile skipping.

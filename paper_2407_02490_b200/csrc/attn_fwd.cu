@@ -31,6 +31,7 @@
 #include "spf_ptx.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace spf {
 
@@ -97,6 +98,23 @@ struct Layout {
 };
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+
+// Debug timeline (spf_debug_attn_trace): per traced CTA, 4 slots per (role, step):
+// role 0 = MMA warp, 1 = softmax warp 2.
+constexpr int kTraceSteps1 = 64;
+__device__ unsigned long long* g_trace1 = nullptr;
+__device__ int g_trace1_ctas = 0;
+#ifndef SPF_TRACE
+#define SPF_TRACE 0
+#endif
+__device__ __forceinline__ void trace1(int role, int step, int ev) {
+  if (!SPF_TRACE) return;
+  unsigned long long* tr = g_trace1;
+  if (tr == nullptr || (int)blockIdx.x >= g_trace1_ctas || step >= kTraceSteps1) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[(((int64_t)blockIdx.x * 3 + role) * kTraceSteps1 + step) * 4 + ev] = t;
+}
 
 // D[tmem] (+)= A[tmem] * B[smem]: P (bf16, K-major, 2 per 32-bit column) times V.
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -424,34 +442,41 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     }
   } else if (warp == 1) {
     // =============================== MMA issuer ================================
-    if (lane == 0) {
+    {  // whole warp, warp-uniform; elected lane issues
       constexpr uint32_t idesc_qk = umma_idesc_bf16(128, kBox, 0, 0);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(128, kD, 0, 1);
-      const uint32_t q_addr = sbase + L::kOffQ;
       const uint32_t tO = tmem + 128;
+      // Descriptors are formed once; per MMA only a constant (and a per-stage) offset is
+      // added to the 14-bit start-address field (smem offsets >> 4, no carry out of it).
+      const uint32_t qlo0 = sw128_lo(sbase + L::kOffQ, 0);
+      const uint32_t klo0 = sw128_lo(sbase + L::kOffK, 0);
+      const uint32_t vlo0 = sw128_lo(sbase + L::kOffV, kBox * 128);
+      constexpr uint32_t dhi = sw128_hi(1024);
+      constexpr uint32_t kStageKV = (uint32_t)(L::kCopies * L::kKBytes);
       mbar_wait(&ctrl->q_full, 0);
       tc_fence_after();
 
       auto issue_pv = [&](int u) {
         const int sv = u % R::kV;
         mbar_wait(&ctrl->p_full, u & 1);
+        if (lane == 0) trace1(0, u, 2);
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
         tc_fence_after();
-        const uint32_t v_addr = sbase + L::kOffV + sv * (L::kCopies * L::kKBytes);
+        const uint32_t vd = vlo0 + ((sv * kStageKV) >> 4);
         const uint32_t tP = tmem + (u & 1) * kBox;  // P(u) overwrote S(u): hi in cols 0..31, lo in 32..63
 #pragma unroll
         for (int k = 0; k < kBox / 16; ++k) {
-          const uint64_t b_hi = umma_desc_sw128(v_addr + k * 2048, kBox * 128, 1024);
-          mma_bf16_ts(tO, tP + k * 8, b_hi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
+          const uint32_t b_hi = vd + ((k * 2048) >> 4);
+          mma_bf16_ts_w2(tO, tP + k * 8, b_hi, dhi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
           if (kSplit) {
-            const uint64_t b_lo = umma_desc_sw128(v_addr + L::kKBytes + k * 2048, kBox * 128, 1024);
-            mma_bf16_ts(tO, tP + k * 8, b_lo, idesc_pv, 1u);
-            mma_bf16_ts(tO, tP + 32 + k * 8, b_hi, idesc_pv, 1u);
+            const uint32_t b_lo = vd + ((L::kKBytes + k * 2048) >> 4);
+            mma_bf16_ts_w2(tO, tP + k * 8, b_lo, dhi, idesc_pv, 1u);
+            mma_bf16_ts_w2(tO, tP + 32 + k * 8, b_hi, dhi, idesc_pv, 1u);
           }
         }
-        mma_commit(&ctrl->pv_done);
-        mma_commit(&ctrl->v_empty[sv]);
-        mma_commit(&ctrl->s_free[u & 1]);
+        mma_commit_w(&ctrl->pv_done);
+        mma_commit_w(&ctrl->v_empty[sv]);
+        mma_commit_w(&ctrl->s_free[u & 1]);
       };
 
       int t = 0;
@@ -465,28 +490,33 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         mbar_wait(&ctrl->k_full[sk], (t / R::kK) & 1);
         mbar_wait(&ctrl->s_free[sb], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k_addr = sbase + L::kOffK + sk * (L::kCopies * L::kKBytes);
+        if (lane == 0) trace1(0, t, 0);
+        const uint32_t kd = klo0 + ((sk * kStageKV) >> 4);
         const uint32_t tS = tmem + sb * kBox;
+        const long long c_qk0 = SPF_TRACE ? clock64() : 0;
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
-          const int atom = k >> 2;
-          const uint32_t koff = (k & 3) * 32;
-          const uint64_t a_hi = umma_desc_sw128(q_addr + atom * (kRows * 128) + koff, 0, 1024);
-          const uint64_t b_hi = umma_desc_sw128(k_addr + atom * (kBox * 128) + koff, 0, 1024);
-          mma_bf16_ss(tS, a_hi, b_hi, idesc_qk, k > 0 ? 1u : 0u);
+          const uint32_t aoff = ((k >> 2) * (kRows * 128) + (k & 3) * 32) >> 4;
+          const uint32_t boff = ((k >> 2) * (kBox * 128) + (k & 3) * 32) >> 4;
+          mma_bf16_ss_w2(tS, qlo0 + aoff, dhi, kd + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
           if (kSplit) {
-            const uint64_t a_lo = umma_desc_sw128(q_addr + L::kQBytes + atom * (kRows * 128) + koff, 0, 1024);
-            const uint64_t b_lo = umma_desc_sw128(k_addr + L::kKBytes + atom * (kBox * 128) + koff, 0, 1024);
-            mma_bf16_ss(tS, a_hi, b_lo, idesc_qk, 1u);
-            mma_bf16_ss(tS, a_lo, b_hi, idesc_qk, 1u);
+            mma_bf16_ss_w2(tS, qlo0 + aoff, dhi, kd + boff + (L::kKBytes >> 4), dhi, idesc_qk, 1u);
+            mma_bf16_ss_w2(tS, qlo0 + aoff + (L::kQBytes >> 4), dhi, kd + boff, dhi, idesc_qk, 1u);
           }
         }
-        mma_commit(&ctrl->s_full[sb]);
-        mma_commit(&ctrl->k_empty[sk]);
+        mma_commit_w(&ctrl->s_full[sb]);
+        mma_commit_w(&ctrl->k_empty[sk]);
+        if (SPF_TRACE && lane == 0) {
+          trace1(0, t, 1);
+          const long long dc = clock64() - c_qk0;
+          if (g_trace1 != nullptr && (int)blockIdx.x < g_trace1_ctas && t < kTraceSteps1)
+            g_trace1[(((int64_t)blockIdx.x * 3 + 2) * kTraceSteps1 + t) * 4 + 0] = (unsigned long long)dc;
+        }
         if (t > 0) issue_pv(t - 1);
+        if (lane == 0 && t > 0) trace1(0, t - 1, 3);
       }
       if (t > 0) issue_pv(t - 1);
-      mma_commit(&ctrl->o_ready);
+      mma_commit_w(&ctrl->o_ready);
     }
     __syncwarp();
   } else {
@@ -500,13 +530,17 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     int t = 0;
     for (;; ++t) {
       const int sd = t % R::kD;
+      const bool tr0 = warp == 2 && lane == 0;
+      if (tr0) trace1(1, t, 0);
       mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
+      if (tr0) trace1(1, t, 1);
       const StepDesc& d = ctrl->desc[sd];
       const int kind = d.kind;
       if (kind == kEnd) break;
       const int sb = t & 1;
       mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
       tc_fence_after();
+      if (tr0) trace1(1, t, 2);
       uint32_t x[kBox];
       tmem_ld32x32b_x64(tmem + lane_off + sb * kBox, x);
       tmem_wait_ld();
@@ -609,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full);
+      if (tr0) trace1(1, t, 3);
     }
     // ---- epilogue: O / l -> global ----
     if (t > 0) {
@@ -707,10 +742,20 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
+int attn1_set_trace(unsigned long long* buf, int n_ctas) {
+  int rc = check_cuda(cudaMemcpyToSymbol(g_trace1, &buf, sizeof(buf)), "trace ptr");
+  if (rc) return rc;
+  return check_cuda(cudaMemcpyToSymbol(g_trace1_ctas, &n_ctas, sizeof(int)), "trace ctas");
+}
+
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream) {
   if (a.B < 2) return set_error(2, "block_size must be >= 2 for the sm_100a kernel (got %d)", a.B);
   if (a.Hkv <= 0 || a.Hq % a.Hkv != 0) return set_error(2, "n_q_heads must be a multiple of n_kv_heads");
-  if (attn2_supported(a)) return launch_sparse_attn2(a, stream);
+  static const int kernel_choice = [] {
+    const char* e = getenv("SPF_ATTN_KERNEL");
+    return e ? atoi(e) : 1;
+  }();
+  if (kernel_choice == 2 && attn2_supported(a)) return launch_sparse_attn2(a, stream);
   if (a.kD == 128) return a.split ? launch_impl<128, true>(a, stream) : launch_impl<128, false>(a, stream);
   if (a.kD == 64) return a.split ? launch_impl<64, true>(a, stream) : launch_impl<64, false>(a, stream);
   return set_error(2, "padded head_dim must be 64 or 128 (got %d)", a.kD);

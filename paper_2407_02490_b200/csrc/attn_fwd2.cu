@@ -84,6 +84,23 @@ struct Layout2 {
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
+// Debug timeline (spf_debug_attn_trace): per traced CTA, kTraceEv 64-bit slots per
+// (role, step): role 0 = MMA, 1 = softmax tile A warp 0, 2 = softmax tile B warp 0.
+constexpr int kTraceSteps = 64, kTraceEv = 4;
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_ctas = 0;
+#ifndef SPF_TRACE
+#define SPF_TRACE 0
+#endif
+__device__ __forceinline__ void trace(int role, int step, int ev) {
+  if (!SPF_TRACE) return;
+  unsigned long long* tr = g_trace;
+  if (tr == nullptr || (int)blockIdx.x >= g_trace_ctas || step >= kTraceSteps) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[(((int64_t)blockIdx.x * 3 + role) * kTraceSteps + step) * kTraceEv + ev] = t;
+}
+
 __device__ __forceinline__ void mma_bf16_ts2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
@@ -485,6 +502,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           const bool next = step_kind(t + 1) != kEnd;
           // tile A: PV(t), then QK(t+1) into the S/P columns PV(t) just consumed (in-order pipe)
           mbar_wait(&ctrl->p_full[0], t & 1);
+          trace(0, t, 0);
           mbar_wait(&ctrl->v_full[t % kVS], (t / kVS) & 1);
           tc_fence_after();
           pv(0, t);
@@ -493,17 +511,19 @@ __global__ void __launch_bounds__(kThreads2, 1)
             tc_fence_after();
             qk(0, t + 1);
           }
+          trace(0, t, 1);
           // tile B
           mbar_wait(&ctrl->p_full[1], t & 1);
+          trace(0, t, 2);
           tc_fence_after();
           pv(1, t);
           mma_commit(&ctrl->v_empty[t % kVS]);
           if (next) {
             qk(1, t + 1);
             mma_commit(&ctrl->k_empty[(t + 1) % kKS]);
-          } else {
-            break;
           }
+          trace(0, t, 3);
+          if (!next) break;
         }
       }
       mma_commit(&ctrl->o_ready);
@@ -526,7 +546,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
     int t = 0;
     for (;; ++t) {
       const int sd = t % kDS;
+      const bool tr0 = (warp & 3) == 0 && lane == 0;
+      if (tr0) trace(1 + tile, t, 3);
       mbar_wait(&ctrl->d_full[sd], (t / kDS) & 1);
+      if (tr0) trace(1 + tile, t, 0);
       const StepDesc2& d = ctrl->desc[sd];
       if (d.b[0].kind == kEnd) break;
       int lo0, hi0, lo1, hi1;
@@ -536,6 +559,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
       mbar_wait(&ctrl->s_full[tile], t & 1);
       tc_fence_after();
+      if (tr0) trace(1 + tile, t, 1);
 
       // half 1 (keys 64..127): load, mask, max; keep in registers
       uint32_t x1[kBox];
@@ -617,6 +641,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full[tile]);
+      if (tr0) trace(1 + tile, t, 2);
     }
     // ---- epilogue: O / l -> global ----
     if (t > 0) {
@@ -691,6 +716,12 @@ int launch2_impl(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
+int attn2_set_trace(unsigned long long* buf, int n_ctas) {
+  int rc = check_cuda(cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)), "trace ptr");
+  if (rc) return rc;
+  return check_cuda(cudaMemcpyToSymbol(g_trace_ctas, &n_ctas, sizeof(int)), "trace ctas");
+}
+
 bool attn2_supported(const AttnArgs& a) { return !a.split && !a.out_f32 && a.B >= 4 && (a.kD == 128 || a.kD == 64); }
 
 int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream) {
@@ -699,3 +730,13 @@ int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace spf
+
+namespace spf {
+int attn1_set_trace(unsigned long long* buf, int n_ctas);
+}
+// Debug only (not in include/spf.h): per-CTA globaltimer trace of the attention kernels.
+extern "C" int spf_debug_attn_trace(void* buf, int n_ctas) {
+  int rc = spf::attn2_set_trace(reinterpret_cast<unsigned long long*>(buf), n_ctas);
+  if (rc) return rc;
+  return spf::attn1_set_trace(reinterpret_cast<unsigned long long*>(buf), n_ctas);
+}

@@ -72,7 +72,10 @@ struct Ctrl {
   uint64_t d_empty[Rings<kSplit>::kD];
   uint64_t s_full[2];
   uint64_t s_free[2];
-  uint64_t p_full;
+  // P(t) written, one barrier per S/P buffer: a softmax warp can run one step ahead
+  // of another, and a single barrier would let its step-(t+1) arrivals complete
+  // step t's phase before the slow warp's P(t) is in TMEM
+  uint64_t p_full[2];
   uint64_t pv_done;
   uint64_t o_ready;  // all PVs retired (committed once after the last one)
   uint32_t tmem_base;
@@ -187,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       mbar_init(&ctrl->s_full[s], 1);
       mbar_init(&ctrl->s_free[s], 1);
     }
-    mbar_init(&ctrl->p_full, 128);
+    mbar_init(&ctrl->p_full[0], 128);
+    mbar_init(&ctrl->p_full[1], 128);
     mbar_init(&ctrl->pv_done, 1);
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
 
       auto issue_pv = [&](int u) {
         const int sv = u % R::kV;
-        mbar_wait(&ctrl->p_full, u & 1);
+        mbar_wait(&ctrl->p_full[u & 1], (u >> 1) & 1);
         if (lane == 0) trace1(0, u, 2);
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
         tc_fence_after();
@@ -624,6 +628,13 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       // O rescale needs PV(t-1) retired.  S(t) being ready implies PV(t-2) retired (QK(t)
       // waited s_free), so pv_done has completed t-1 or t phases: the parity wait for
       // phase t-1 cannot alias.  tcgen05.ld/st are warp-collective: decide per warp.
+#ifndef SPF_PV_WAIT_EVERY_STEP
+#define SPF_PV_WAIT_EVERY_STEP 0
+#endif
+      if (SPF_PV_WAIT_EVERY_STEP && t > 0) {
+        mbar_wait(&ctrl->pv_done, (t - 1) & 1);
+        tc_fence_after();
+      }
       if (t > 0 && __any_sync(0xffffffffu, rescale)) {
         mbar_wait(&ctrl->pv_done, (t - 1) & 1);
         tc_fence_after();
@@ -642,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&ctrl->p_full);
+      mbar_arrive(&ctrl->p_full[sb]);
       if (tr0) trace1(1, t, 3);
     }
     // ---- epilogue: O / l -> global ----

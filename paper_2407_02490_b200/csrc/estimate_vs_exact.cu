@@ -51,6 +51,8 @@ struct ExArgs {
   double2* row_ml;         // [n_heads][L]
   double* vscore;          // [n_heads][S]
   double* sscore;          // [n_heads][S]
+  int32_t* list;           // fallback: significant items (h * n_kblk + kb) of the flagged heads
+  int32_t* list_count;     // number of entries in list (device)
 };
 
 template <typename T>
@@ -80,13 +82,31 @@ __device__ void score_tile(ExSmem& sm, const T* qh, const T* kh, int r0, int n_r
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const bool vec = (d % 8) == 0 && sizeof(T) == 2;  // 16-byte loads of 8 bf16
   for (int c0 = 0; c0 < d; c0 += kDc) {
     __syncthreads();
-    for (int e = tid; e < kRowT * kDc; e += kThreads) {
-      const int r = e / kDc, c = e % kDc;
-      const bool okc = c0 + c < d;
-      sm.At[c * kLd + r] = (okc && r < n_rows_valid) ? ld_f64(qh + (int64_t)(r0 + r) * d + c0 + c) : 0.0;
-      sm.Bt[c * kLd + r] = (okc && k0 + r < S) ? ld_f64(kh + (int64_t)(k0 + r) * d + c0 + c) : 0.0;
+    if (vec) {
+      // one 16-byte load per thread per operand: row r = tid / 4, dims c0 + 8 (tid % 4) .. + 7
+      const int r = tid >> 2, cc = (tid & 3) * 8;
+      if (cc < kDc) {
+        int4 qa = make_int4(0, 0, 0, 0), kbv = make_int4(0, 0, 0, 0);
+        if (c0 + cc < d && r < n_rows_valid) qa = *reinterpret_cast<const int4*>(qh + (int64_t)(r0 + r) * d + c0 + cc);
+        if (c0 + cc < d && k0 + r < S) kbv = *reinterpret_cast<const int4*>(kh + (int64_t)(k0 + r) * d + c0 + cc);
+        const __nv_bfloat16* qv = reinterpret_cast<const __nv_bfloat16*>(&qa);
+        const __nv_bfloat16* kv = reinterpret_cast<const __nv_bfloat16*>(&kbv);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sm.At[(cc + u) * kLd + r] = (double)__bfloat162float(qv[u]);
+          sm.Bt[(cc + u) * kLd + r] = (double)__bfloat162float(kv[u]);
+        }
+      }
+    } else {
+      for (int e = tid; e < kRowT * kDc; e += kThreads) {
+        const int r = e / kDc, c = e % kDc;
+        const bool okc = c0 + c < d;
+        sm.At[c * kLd + r] = (okc && r < n_rows_valid) ? ld_f64(qh + (int64_t)(r0 + r) * d + c0 + c) : 0.0;
+        sm.Bt[c * kLd + r] = (okc && k0 + r < S) ? ld_f64(kh + (int64_t)(k0 + r) * d + c0 + c) : 0.0;
+      }
     }
     __syncthreads();
     const int cn = min(kDc, d - c0);
@@ -120,6 +140,33 @@ __device__ bool item_significant(const ExArgs& a, int h, int k0) {
   return __syncthreads_or(sig) != 0;
 }
 
+// Fallback preparation (tile_max given): one warp per (flagged head, 64-key item).
+// Zeroes the item's slash entries, writes the outputs of items whose probabilities
+// are all exactly 0 in fp32 (stats (-inf, 0), vertical 0) and lists the others.
+__global__ void vs_exact_prep_kernel(const ExArgs a) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)a.n_heads * a.n_kblk) return;
+  const int h = (int)(w / a.n_kblk), kb = (int)(w % a.n_kblk);
+  if (a.gate != nullptr && a.gate[h] == 0) return;
+  const int S = a.S, k0 = kb * a.KB;
+  const int n_t = (S + 127) / 128, t = k0 / 128;
+  int sig = 0;
+  for (int i = lane; i < 64; i += 32) {
+    const float tm = a.tile_max[((int64_t)h * 64 + i) * n_t + t];
+    const float mc = a.row_mc[(int64_t)h * 64 + i];
+    sig |= !(tm * a.c - mc < -152.f);
+  }
+  sig = __any_sync(0xffffffffu, sig);
+  for (int o = k0 + lane; o < min(k0 + a.KB, S); o += 32) a.sscore[(int64_t)h * S + o] = 0.0;
+  if (sig) {
+    if (lane == 0) a.list[atomicAdd(a.list_count, 1)] = (int32_t)w;
+  } else {
+    for (int i = lane; i < a.L; i += 32) a.stats[((int64_t)h * a.L + i) * a.n_kblk + kb] = make_double2(-INFINITY, 0.0);
+    for (int j = k0 + lane; j < min(k0 + a.KB, S); j += 32) a.vscore[(int64_t)h * S + j] = 0.0;
+  }
+}
+
 template <typename T, int kPass>
 __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                             const ExArgs a) {
@@ -132,20 +179,30 @@ __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restri
   const int n_rt = (L + kRowT - 1) / kRowT;
   // items (head, key block) interleaved head-fastest, so the significant blocks of every
   // flagged head (often a narrow band of keys) spread over all CTAs
-  const int64_t n_items = (int64_t)a.n_heads * a.n_kblk;
+  // with a prepared list (fallback) only its items are visited; the prep kernel
+  // already zeroed the slash vector and wrote the skipped items' outputs
+  const bool listed = a.list != nullptr;
+  const int64_t n_items = listed ? (int64_t)*a.list_count : (int64_t)a.n_heads * a.n_kblk;
   for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const int h = (int)(w % a.n_heads);
-    const int kb = (int)(w / a.n_heads);
-    if (a.gate != nullptr && a.gate[h] == 0) continue;
+    int h, kb;
+    if (listed) {
+      const int it = a.list[w];
+      h = it / a.n_kblk;
+      kb = it % a.n_kblk;
+    } else {
+      h = (int)(w % a.n_heads);
+      kb = (int)(w / a.n_heads);
+    }
+    if (!listed && a.gate != nullptr && a.gate[h] == 0) continue;
     const int qh_id = a.head_ids ? a.head_ids[h] : h;
     const T* qh = q + ((int64_t)qh_id * S + (S - L)) * d;
     const T* kh = k + (int64_t)(qh_id / a.hpk) * S * d;
     {
       const int k0 = kb * KB;
-      if (kPass == 1) {  // zero this item's share of the slash vector (pass 2 accumulates into it)
+      if (kPass == 1 && !listed) {  // zero this item's share of the slash vector (pass 2 accumulates into it)
         for (int o = k0 + tid; o < min(k0 + KB, S); o += kThreads) a.sscore[(int64_t)h * S + o] = 0.0;
       }
-      const bool sig = item_significant(a, h, k0);
+      const bool sig = listed || item_significant(a, h, k0);
       if (!sig) {
         if (kPass == 1) {
           for (int i = tid; i < L; i += kThreads)
@@ -315,7 +372,7 @@ size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q) {
   const int KB = kb_for(last_q);
   const size_t n_kblk = (seq_len + KB - 1) / KB;
   return al256((size_t)n_heads * last_q * n_kblk * 16) + al256((size_t)n_heads * last_q * 16) +
-         2 * al256((size_t)n_heads * seq_len * 8);
+         2 * al256((size_t)n_heads * seq_len * 8) + al256((size_t)n_heads * n_kblk * 4) + al256(4);
 }
 
 int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
@@ -346,6 +403,8 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
   a.row_ml = reinterpret_cast<double2*>(take((size_t)n_heads * L * 16));
   a.vscore = vscore ? vscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
+  int32_t* list = reinterpret_cast<int32_t*>(take((size_t)n_heads * a.n_kblk * 4));
+  int32_t* list_count = reinterpret_cast<int32_t*>(take(4));
   const size_t smem = sizeof(ExSmem) + (size_t)(2 * a.KB + L - 1) * 8;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)a.n_kblk * n_heads, 148 * 4));
   int rc;
@@ -357,6 +416,14 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
                          "vs exact smem")))
       return rc;
     note_launches(4);  // pass A, combine, pass B, top-k
+    if (a.tile_max != nullptr) {
+      if ((rc = check_cuda(cudaMemsetAsync(list_count, 0, 4, st), "list count"))) return rc;
+      a.list = list;
+      a.list_count = list_count;
+      const int64_t warps = (int64_t)n_heads * a.n_kblk;
+      note_launches(1);
+      vs_exact_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+    }
     k1<<<grid, kThreads, smem, st>>>(qq, kk, a);
     vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
     k2<<<grid, kThreads, smem, st>>>(qq, kk, a);

@@ -43,6 +43,13 @@ constexpr int kThreads = 192;
 
 enum : int { kTile = 0, kChip = 1, kEnd = 2 };
 
+#ifndef SPF_EXP_EMU1
+#define SPF_EXP_EMU1 0  // 0: all on MUFU (emulating 1 in 4 pairs measured 8% slower: issue-bound softmax)
+#endif
+// every kEmu1-th pair of exponentials of the bf16 path is computed on the FMA pipe
+// (exp2_poly_x2) instead of MUFU: the two CTAs' softmax warps share each SMSP's MUFU
+constexpr int kEmu1 = SPF_EXP_EMU1;
+
 struct StepDesc {
   unsigned long long segmask;
   int box;      // tile: first key of the loaded box
@@ -603,9 +610,15 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
 #pragma unroll
       for (int j = 0; j < kBox; j += 2) {
         const uint64_t y = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
-        float y0, y1;
-        unpack_f32x2(y, y0, y1);
-        const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+        float p0, p1;
+        if (!kSplit && kEmu1 > 0 && ((j >> 1) % (kEmu1 > 0 ? kEmu1 : 1)) == kEmu1 - 1) {
+          unpack_f32x2(exp2_poly_x2(y), p0, p1);  // part of the exponentials on the FMA pipe
+        } else {
+          float y0, y1;
+          unpack_f32x2(y, y0, y1);
+          p0 = ex2_approx(y0);
+          p1 = ex2_approx(y1);
+        }
         const uint64_t pp = pack_f32x2(p0, p1);
         switch ((j >> 1) & 3) {
           case 0: s0 = fadd2(s0, pp); break;

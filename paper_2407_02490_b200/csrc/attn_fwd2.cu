@@ -40,6 +40,12 @@ constexpr int kWarpLoad = 8, kWarpMma = 9;
 // registers per thread after setmaxnreg: the two softmax warpgroups grow, the
 // producer warpgroup shrinks (8*32*184 + 4*32*120 <= 65536; both spill-free)
 constexpr int kRegsSoftmax = 184, kRegsProducer = 120;
+#ifndef SPF_EXP_EMU
+#define SPF_EXP_EMU 0  // 0: all exponentials on MUFU (measured faster for this kernel)
+#endif
+// every kEmu-th pair of exponentials is computed by exp2_poly_x2 on the FMA pipe
+// (the two softmax warpgroups share each SMSP's MUFU; the FA4 balance)
+constexpr int kEmu = SPF_EXP_EMU;
 
 enum : int { kNone = 0, kTile = 1, kChip = 2, kEnd = 3 };
 
@@ -603,9 +609,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
       // keys 64..127 -> P in cols 96..127 (their S columns are already in registers)
 #pragma unroll
       for (int j = 0; j < kBox; j += 2) {
-        float y0, y1;
-        unpack_f32x2(ffma2(pack_f32x2(u2f(x1[j]), u2f(x1[j + 1])), c2, m2), y0, y1);
-        const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+        const uint64_t y = ffma2(pack_f32x2(u2f(x1[j]), u2f(x1[j + 1])), c2, m2);
+        float p0, p1;
+        if (kEmu > 0 && ((j >> 1) % (kEmu > 0 ? kEmu : 1)) == kEmu - 1) {  // part of the exponentials on the FMA pipe
+          unpack_f32x2(exp2_poly_x2(y), p0, p1);
+        } else {
+          float y0, y1;
+          unpack_f32x2(y, y0, y1);
+          p0 = ex2_approx(y0);
+          p1 = ex2_approx(y1);
+        }
         if ((j >> 1) & 1) s1 = fadd2(s1, pack_f32x2(p0, p1)); else s0 = fadd2(s0, pack_f32x2(p0, p1));
         ph[j >> 1] = pack_bf16x2(p0, p1);
       }
@@ -613,9 +626,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
       // keys 0..63 -> P in cols 0..31
 #pragma unroll
       for (int j = 0; j < kBox; j += 2) {
-        float y0, y1;
-        unpack_f32x2(ffma2(pack_f32x2(u2f(x0[j]), u2f(x0[j + 1])), c2, m2), y0, y1);
-        const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+        const uint64_t y = ffma2(pack_f32x2(u2f(x0[j]), u2f(x0[j + 1])), c2, m2);
+        float p0, p1;
+        if (kEmu > 0 && ((j >> 1) % (kEmu > 0 ? kEmu : 1)) == kEmu - 1) {
+          unpack_f32x2(exp2_poly_x2(y), p0, p1);
+        } else {
+          float y0, y1;
+          unpack_f32x2(y, y0, y1);
+          p0 = ex2_approx(y0);
+          p1 = ex2_approx(y1);
+        }
         if ((j >> 1) & 1) s3 = fadd2(s3, pack_f32x2(p0, p1)); else s2 = fadd2(s2, pack_f32x2(p0, p1));
         ph[j >> 1] = pack_bf16x2(p0, p1);
       }

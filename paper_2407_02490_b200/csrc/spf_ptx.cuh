@@ -247,6 +247,38 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+// 2^y for two packed floats on the FMA pipe (no MUFU): y = j + f with j = rint(y),
+// f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5),
+// 2^j added to the exponent bits.  Inputs below -126 (incl. -inf) give exactly 0.
+__device__ __forceinline__ uint64_t exp2_poly_x2(uint64_t y2) {
+  float y0, y1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(y0), "=f"(y1) : "l"(y2));
+  const float c0 = fmaxf(y0, -127.f), c1 = fmaxf(y1, -127.f);
+  uint64_t yc, r, jf, f, p;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(yc) : "f"(c0), "f"(c1));
+  const uint64_t magic = 0x4B4000004B400000ull;      // 1.5 * 2^23 (x2)
+  const uint64_t neg_magic = 0xCB400000CB400000ull;  // -1.5 * 2^23 (x2)
+  const uint64_t neg_one = 0xBF800000BF800000ull;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(yc), "l"(magic));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(jf) : "l"(r), "l"(neg_magic));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(jf), "l"(neg_one), "l"(yc));
+  const uint64_t k3 = 0x3D61FBAF3D61FBAFull;  // 0.0551716648
+  const uint64_t k2 = 0x3E786F0D3E786F0Dull;  // 0.2426111251
+  const uint64_t k1 = 0x3F31798D3F31798Dull;  // 0.6932609677
+  const uint64_t k0 = 0x3F7FFB493F7FFB49ull;  // 0.9999280572
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(k3), "l"(k2));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(p), "l"(k1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(p), "l"(k0));
+  uint32_t p0, p1, r0, r1;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(p));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(r0), "=r"(r1) : "l"(r));
+  const uint32_t e0 = (y0 < -126.f) ? 0u : p0 + (r0 << 23);
+  const uint32_t e1 = (y1 < -126.f) ? 0u : p1 + (r1 << 23);
+  uint64_t out;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(out) : "r"(e0), "r"(e1));
+  return out;
+}
+
 __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   uint64_t d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));

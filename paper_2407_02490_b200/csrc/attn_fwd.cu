@@ -438,14 +438,27 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     StepInfo pend;
     bool have_pend = false;
     int t = 0;
+    long long tl_gen = 0, tl_k = 0, tl_v = 0;
     while (true) {
       StepInfo st;
+      long long c0 = SPF_TRACE ? clock64() : 0;
       next_step(st);
+      long long c1 = SPF_TRACE ? clock64() : 0;
       if (st.kind != kEnd) issue_k(have_pend ? t + 1 : t, st);
       else write_desc(have_pend ? t + 1 : t, st);  // end marker through the descriptor ring
+      long long c2 = SPF_TRACE ? clock64() : 0;
       if (have_pend) {
         issue_v(t, pend);
         ++t;
+      }
+      if (SPF_TRACE) {
+        tl_gen += c1 - c0;
+        tl_k += c2 - c1;
+        tl_v += clock64() - c2;
+        if (lane == 0 && t == 48 && g_trace1 != nullptr && (int)blockIdx.x < g_trace1_ctas) {
+          unsigned long long* tr = g_trace1 + (((int64_t)blockIdx.x * 3 + 2) * kTraceSteps1 + 60) * 4;
+          tr[0] = tl_gen; tr[1] = tl_k; tr[2] = tl_v;
+        }
       }
       if (st.kind == kEnd) break;
       pend = st;

@@ -32,7 +32,6 @@ namespace {
 
 constexpr int kTile = 64;       // rows x keys per score tile
 constexpr int kScoreThreads = 256;
-constexpr int kLd = kTile + 2;  // padded smem leading dimension (doubles)
 
 template <typename T>
 __device__ __forceinline__ double ld_as_double(const T* p) {
@@ -43,83 +42,65 @@ __device__ __forceinline__ double ld_as_double<__nv_bfloat16>(const __nv_bfloat1
   return static_cast<double>(__bfloat162float(*p));
 }
 
-// Generic fp64 tile: C[a, b] = scale * A[a] . B[b] for a 64x64 tile.
-//   VS mode: A = q tail rows, abs row = a_abs0 + a; mask b > abs row; emits partial stats.
-//   BS mode: A = pooled q rows (row index = block r), B = pooled k rows; skips tiles above the diagonal.
-template <typename TA, typename TB, bool kVS>
-__global__ void __launch_bounds__(kScoreThreads) score_tile_kernel(
-    const TA* __restrict__ A, const TB* __restrict__ Bm, const int32_t* __restrict__ head_ids, int heads_per_kv,
-    int64_t a_head_stride, int64_t b_head_stride, int a_row0, int n_a, int n_b, int d, double scale, int a_abs0,
-    double* __restrict__ out, int64_t out_head_stride, double2* __restrict__ stats, int n_kblk) {
-  extern __shared__ double smd[];
-  double* At = smd;               // [d][kLd]
-  double* Bt = smd + d * kLd;     // [d][kLd]
+// Block-Sparse pooled scores, fp64: out[r][c] = scale * qp[r] . kp[c] for the block-causal
+// triangle (c <= r), one 64x64 tile per CTA.  d is staged in 32-wide chunks (two CTAs
+// per SM); each thread owns rows 4 tr .. 4 tr + 3 and columns tk + 16 y, so the column
+// operand is read conflict-free (16 consecutive doubles per warp load).
+constexpr int kDc = 32;
+constexpr int kLdc = 68;
+
+__global__ void __launch_bounds__(kScoreThreads, 2) bs_score_kernel(
+    const float* __restrict__ qp, const float* __restrict__ kp, const int32_t* __restrict__ head_ids,
+    int heads_per_kv, int N, int d, double scale, double* __restrict__ out) {
+  __shared__ double At[kDc * kLdc];
+  __shared__ double Bt[kDc * kLdc];
   const int hi = blockIdx.z;
   const int h = head_ids ? head_ids[hi] : hi;
   const int kvh = h / heads_per_kv;
   const int bt = blockIdx.x, at = blockIdx.y;
-  if (!kVS && bt > at) return;  // BS: block-causal triangle only
+  if (bt > at) return;  // block-causal triangle only
   const int a0 = at * kTile, b0 = bt * kTile;
-  const TA* Ah = A + (int64_t)h * a_head_stride + (int64_t)a_row0 * d;
-  const TB* Bh = Bm + (int64_t)kvh * b_head_stride;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kTile * d; e += kScoreThreads) {
-    const int r = e / d, c = e % d;
-    At[c * kLd + r] = (a0 + r < n_a) ? ld_as_double(Ah + (int64_t)(a0 + r) * d + c) : 0.0;
-    Bt[c * kLd + r] = (b0 + r < n_b) ? ld_as_double(Bh + (int64_t)(b0 + r) * d + c) : 0.0;
-  }
-  __syncthreads();
-  const int tr = tid >> 4, tk = tid & 15;
+  const float* Ah = qp + (int64_t)h * N * d;
+  const float* Bh = kp + (int64_t)kvh * N * d;
+  const int tid = threadIdx.x, tr = tid >> 4, tk = tid & 15;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (int c = 0; c < d; ++c) {
-    const double2 qa = *reinterpret_cast<const double2*>(At + c * kLd + 4 * tr);
-    const double2 qb = *reinterpret_cast<const double2*>(At + c * kLd + 4 * tr + 2);
-    const double2 ka = *reinterpret_cast<const double2*>(Bt + c * kLd + 4 * tk);
-    const double2 kb = *reinterpret_cast<const double2*>(Bt + c * kLd + 4 * tk + 2);
-    const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
-    const double kv[4] = {ka.x, ka.y, kb.x, kb.y};
+  for (int c0 = 0; c0 < d; c0 += kDc) {
+    __syncthreads();
+    for (int e = tid; e < kTile * kDc; e += kScoreThreads) {
+      const int r = e / kDc, c = e % kDc;
+      const bool okc = c0 + c < d;
+      At[c * kLdc + r] = (okc && a0 + r < N) ? (double)Ah[(int64_t)(a0 + r) * d + c0 + c] : 0.0;
+      Bt[c * kLdc + r] = (okc && b0 + r < N) ? (double)Bh[(int64_t)(b0 + r) * d + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    const int cn = min(kDc, d - c0);
+#pragma unroll 4
+    for (int c = 0; c < cn; ++c) {
+      const double2 qa = *reinterpret_cast<const double2*>(At + c * kLdc + 4 * tr);
+      const double2 qb = *reinterpret_cast<const double2*>(At + c * kLdc + 4 * tr + 2);
+      const double qv[4] = {qa.x, qa.y, qb.x, qb.y};
+      double kv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int y = 0; y < 4; ++y) kv[y] = Bt[c * kLdc + tk + 16 * y];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fma(qv[i], kv[j], acc[i][j]);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[i][y] = fma(qv[i], kv[y], acc[i][y]);
+    }
   }
-  double* outh = out + (int64_t)hi * out_head_stride;
+  double* outh = out + (int64_t)hi * N * N;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int a = a0 + 4 * tr + i;
-    double s[4];
-    double mx = -INFINITY;
+    if (a >= N) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int b = b0 + 4 * tk + j;
-      s[j] = scale * acc[i][j];
-      const bool valid = (a < n_a) && (b < n_b) && (kVS ? (b <= a_abs0 + a) : (b <= a));
-      if (valid) mx = fmax(mx, s[j]);
-      else s[j] = -INFINITY;
-    }
-    if (a < n_a) {
-      double* orow = outh + (int64_t)a * n_b + b0 + 4 * tk;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (b0 + 4 * tk + j < n_b) orow[j] = s[j];
-    }
-    if (kVS) {
-      // partial (max, sum exp) over this tile's 64 keys, fixed butterfly order
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      double l = 0.0;
-      if (mx != -INFINITY) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (s[j] != -INFINITY) l += exp(s[j] - mx);
-      }
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-      if (tk == 0 && a < n_a) stats[((int64_t)hi * n_a + a) * n_kblk + bt] = make_double2(mx, l);
+    for (int y = 0; y < 4; ++y) {
+      const int b = b0 + tk + 16 * y;
+      if (b < N) outh[(int64_t)a * N + b] = (b <= a) ? scale * acc[i][y] : -INFINITY;
     }
   }
 }
@@ -200,20 +181,15 @@ int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, cons
   int rc;
   {
     const int64_t tq = (int64_t)Hq * N * d, tk = (int64_t)Hkv * N * d;
-    note_launches(4);  // pool q, pool k, block scores, row top-k
+    note_launches(3);  // pool q, pool k, row top-k (+1 block scores below)
     pool_kernel<T><<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
     pool_kernel<T><<<(unsigned)((tk + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
     if ((rc = check_cuda(cudaGetLastError(), "bs pool"))) return rc;
   }
-  const size_t smem = (size_t)2 * d * kLd * sizeof(double);
-  auto kern = score_tile_kernel<float, float, false>;
-  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                       "bs score smem attr")))
-    return rc;
   const int nt = (N + kTile - 1) / kTile;
-  kern<<<dim3((unsigned)nt, (unsigned)nt, (unsigned)n_heads), kScoreThreads, smem, st>>>(
-      qp, kp, head_ids, Hq / Hkv, (int64_t)N * d, (int64_t)N * d, 0, N, N, d, 1.0 / sqrt((double)d), 0, sc,
-      (int64_t)N * N, nullptr, 0);
+  note_launches(1);
+  bs_score_kernel<<<dim3((unsigned)nt, (unsigned)nt, (unsigned)n_heads), kScoreThreads, 0, st>>>(
+      qp, kp, head_ids, Hq / Hkv, N, d, 1.0 / sqrt((double)d), sc);
   if ((rc = check_cuda(cudaGetLastError(), "bs score"))) return rc;
   const size_t rsmem = (size_t)N * sizeof(float);
   if ((rc = check_cuda(cudaFuncSetAttribute(bs_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem),

@@ -1,0 +1,69 @@
+// MUFU.EX2 throughput on one SM: warps x independent ex2.approx chains.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb_mufu benchmarks/mb_mufu.cu && ./mb_mufu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int kChains>
+__global__ void ex2_kernel(float* out, int iters, long long* cyc) {
+  float x[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) x[c] = -0.001f * (threadIdx.x + c);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[c]));
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += x[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// packed FFMA2 throughput for comparison
+__global__ void ffma2_kernel(float* out, int iters, long long* cyc) {
+  unsigned long long x[8];
+  for (int c = 0; c < 8; ++c) x[c] = 0x3f8000003f800000ull + c;
+  const unsigned long long m = 0x3f7fffff3f7fffffull, a = 0x3c0000003c000000ull;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(m), "l"(a));
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  unsigned long long s = 0;
+  for (int c = 0; c < 8; ++c) s += x[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+int main() {
+  float* out;
+  long long* cyc;
+  cudaMalloc(&out, 1 << 24);
+  cudaMalloc(&cyc, 4096 * 8);
+  const int iters = 4096;
+  for (int warps : {1, 2, 4, 8, 16}) {
+    ex2_kernel<8><<<1, warps * 32>>>(out, iters, cyc);
+    cudaDeviceSynchronize();
+    long long c;
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    const double ops = (double)warps * 32 * 8 * iters;
+    printf("ex2   warps=%2d  %.2f lanes/clk/SM  (%.2f cyc per warp-instr per SMSP)\n", warps, ops / c,
+           (double)c / ((double)warps * 8 * iters) * (warps >= 4 ? 4 : warps));
+  }
+  for (int warps : {4, 8, 16}) {
+    ffma2_kernel<<<1, warps * 32>>>(out, iters, cyc);
+    cudaDeviceSynchronize();
+    long long c;
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    const double ops = (double)warps * 32 * 8 * iters;
+    printf("ffma2 warps=%2d  %.2f packed-lanes/clk/SM\n", warps, ops / c);
+  }
+  return 0;
+}

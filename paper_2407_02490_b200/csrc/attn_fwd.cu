@@ -39,16 +39,9 @@ namespace {
 
 constexpr int kRows = 128;   // query rows per CTA
 constexpr int kBox = 64;     // keys per step
-constexpr int kThreads = 192;
 
 enum : int { kTile = 0, kChip = 1, kEnd = 2 };
 
-#ifndef SPF_EXP_EMU1
-#define SPF_EXP_EMU1 0  // 0: all on MUFU (emulating 1 in 4 pairs measured 8% slower: issue-bound softmax)
-#endif
-// every kEmu1-th pair of exponentials of the bf16 path is computed on the FMA pipe
-// (exp2_poly_x2) instead of MUFU: the two CTAs' softmax warps share each SMSP's MUFU
-constexpr int kEmu1 = SPF_EXP_EMU1;
 
 struct StepDesc {
   unsigned long long segmask;
@@ -61,6 +54,24 @@ struct StepDesc {
 // Ring depths: K is loaded one step ahead of V and released as soon as its
 // QK^T completes, so it gets the deeper ring; V (and the step descriptor that
 // travels with it) is released after PV.
+// TMEM columns (256 per CTA, two CTAs per SM): bf16 path = S [0,64) single-buffered,
+// P(t) in [64 + 32*(t&1), +32) (separate, so QK(t+1) only waits for the softmax to READ
+// S(t), not for PV(t)), O [128,256).  The split (fp32 I/O) path needs 64 P columns per
+// step and keeps P over S with two S buffers: S/P [0,64) and [64,128), O [128,256).
+template <bool kSplit>
+constexpr bool kSepP = !kSplit;
+
+// softmax warps per TMEM lane quarter.  2 (each thread exponentiates half a row, both
+// halves read the whole row for the max) was measured 14% slower than 1 on C2: more
+// warps per SMSP delay the MMA and loader warps more than the shorter softmax helps.
+#ifndef SPF_SOFT_HALVES
+#define SPF_SOFT_HALVES 1
+#endif
+template <bool kSplit>
+constexpr int kSoftHalves = kSplit ? 1 : SPF_SOFT_HALVES;
+template <bool kSplit>
+constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
+
 template <bool kSplit>
 struct Rings {
   static constexpr int kK = kSplit ? 2 : 3;
@@ -114,6 +125,12 @@ __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 constexpr int kTraceSteps1 = 64;
 __device__ unsigned long long* g_trace1 = nullptr;
 __device__ int g_trace1_ctas = 0;
+// Bottleneck experiments (timing only, results are garbage): 1 = synthetic loader
+// schedule without list reads, 2 = softmax skipped, 3 = QK MMAs skipped, 4 = PV MMAs skipped,
+// 5 = K/V tile loads skipped (barriers still flip), 6 = 2 + 5.
+#ifndef SPF_EXPT
+#define SPF_EXPT 0
+#endif
 #ifndef SPF_TRACE
 #define SPF_TRACE 0
 #endif
@@ -148,7 +165,7 @@ struct StepInfo {
 };
 
 template <int kD, bool kSplit>
-__global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
+__global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_q2,
                            const __grid_constant__ CUtensorMap tm_k2, const __grid_constant__ CUtensorMap tm_v2,
@@ -191,14 +208,15 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     }
     for (int s = 0; s < R::kD; ++s) {
       mbar_init(&ctrl->d_full[s], 1);
-      mbar_init(&ctrl->d_empty[s], 4);  // one arrival per softmax warp
+      mbar_init(&ctrl->d_empty[s], 4 * kSoftHalves<kSplit>);  // one arrival per softmax warp
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ctrl->s_full[s], 1);
-      mbar_init(&ctrl->s_free[s], 1);
+      // separate-P layout: S is released by the softmax warps once read (one arrival each)
+      mbar_init(&ctrl->s_free[s], kSepP<kSplit> ? 4 * kSoftHalves<kSplit> : 1);
     }
-    mbar_init(&ctrl->p_full[0], 128);
-    mbar_init(&ctrl->p_full[1], 128);
+    mbar_init(&ctrl->p_full[0], 128 * kSoftHalves<kSplit>);
+    mbar_init(&ctrl->p_full[1], 128 * kSoftHalves<kSplit>);
     mbar_init(&ctrl->pv_done, 1);
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
@@ -267,7 +285,19 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       c0 = p.col_offsets[row0];
       cend = p.col_offsets[row0 + 1];
     }
+    int expt_left = (SPF_EXPT == 1 && G > 0) ? (int)(p.tile_offsets[row0 + 1] - p.tile_offsets[row0]) : 0;
     auto next_step = [&](StepInfo& st) {
+      if (SPF_EXPT == 1) {
+        if (expt_left-- > 0) {
+          st.kind = kTile;
+          st.box = max(0, R0 + kRows - kBox - kBox * expt_left);
+          st.width = kBox;
+          st.mask = ~0ull;
+        } else {
+          st.kind = kEnd;
+        }
+        return;
+      }
       if (phase == 0) {
         if (!tile_open) {
           const int best = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
@@ -398,7 +428,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       uint8_t* kst = smem + L::kOffK + sk * (L::kCopies * L::kKBytes);
       if (lane == 0) mbar_wait(&ctrl->k_empty[sk], ((t / R::kK) & 1) ^ 1);
       __syncwarp();
-      if (st.kind == kTile) {
+      if (st.kind == kTile && (SPF_EXPT == 5 || SPF_EXPT == 6)) {
+        if (lane == 0) mbar_arrive(&ctrl->k_full[sk]);
+      } else if (st.kind == kTile) {
         if (lane == 0) {
           mbar_arrive_expect_tx(&ctrl->k_full[sk], L::kTxKV);
 #pragma unroll
@@ -422,6 +454,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       __syncwarp();
       if (st.kind == kChip) {
         gather(vst, vb, vb2, st);
+        if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
+      } else if (SPF_EXPT == 5 || SPF_EXPT == 6) {
         if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
       } else if (lane == 0) {
         mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
@@ -487,9 +521,10 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
         tc_fence_after();
         const uint32_t vd = vlo0 + ((sv * kStageKV) >> 4);
-        const uint32_t tP = tmem + (u & 1) * kBox;  // P(u) overwrote S(u): hi in cols 0..31, lo in 32..63
+        // P(u): own columns (separate-P) or over S(u) (split: hi in cols 0..31, lo in 32..63)
+        const uint32_t tP = kSepP<kSplit> ? tmem + kBox + (u & 1) * (kBox / 2) : tmem + (u & 1) * kBox;
 #pragma unroll
-        for (int k = 0; k < kBox / 16; ++k) {
+        for (int k = 0; k < (SPF_EXPT == 4 ? 0 : kBox / 16); ++k) {
           const uint32_t b_hi = vd + ((k * 2048) >> 4);
           mma_bf16_ts_w2(tO, tP + k * 8, b_hi, dhi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
           if (kSplit) {
@@ -500,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         }
         mma_commit_w(&ctrl->pv_done);
         mma_commit_w(&ctrl->v_empty[sv]);
-        mma_commit_w(&ctrl->s_free[u & 1]);
+        if (!kSepP<kSplit>) mma_commit_w(&ctrl->s_free[u & 1]);
       };
 
       int t = 0;
@@ -510,16 +545,20 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
         const int kind = *reinterpret_cast<volatile short*>(&ctrl->desc[sd].kind);
         if (kind == kEnd) break;
         const int sk = t % R::kK;
-        const int sb = t & 1;
+        const int sb = kSepP<kSplit> ? 0 : t & 1;
         mbar_wait(&ctrl->k_full[sk], (t / R::kK) & 1);
-        mbar_wait(&ctrl->s_free[sb], ((t >> 1) & 1) ^ 1);
+        if (kSepP<kSplit>) {
+          if (t > 0) mbar_wait(&ctrl->s_free[0], (t - 1) & 1);  // softmax(t-1) has read S
+        } else {
+          mbar_wait(&ctrl->s_free[sb], ((t >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
         if (lane == 0) trace1(0, t, 0);
         const uint32_t kd = klo0 + ((sk * kStageKV) >> 4);
         const uint32_t tS = tmem + sb * kBox;
         const long long c_qk0 = SPF_TRACE ? clock64() : 0;
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
+        for (int k = 0; k < (SPF_EXPT == 3 ? 0 : kD / 16); ++k) {
           const uint32_t aoff = ((k >> 2) * (kRows * 128) + (k & 3) * 32) >> 4;
           const uint32_t boff = ((k >> 2) * (kBox * 128) + (k & 3) * 32) >> 4;
           mma_bf16_ss_w2(tS, qlo0 + aoff, dhi, kd + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
@@ -545,7 +584,18 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
     __syncwarp();
   } else {
     // =============================== softmax warps =============================
+    // kHalves warps per TMEM lane quarter; thread <-> (row, key half).  Every thread
+    // reads its row's whole 64-key S slice (the row max needs all of it) but
+    // exponentiates and writes P for its own kCols keys only, keeps l for its half
+    // (the halves agree on m bit for bit) and rescales / stores its kD / kHalves
+    // columns of O.  Two halves = twice the warps to hide the exp/FMA latency chain.
+    constexpr int kHalves = kSoftHalves<kSplit>;
+    constexpr int kCols = kBox / kHalves;
+    constexpr int kOCols = kD / kHalves;
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int c0 = half * kCols;       // first key (S column) of this thread's half
+    const int oc0 = half * kOCols;     // first O column of this thread's half
     const int row = quarter * 32 + lane;
     const int q = R0 + row;
     const int seg = (q < S) ? (q / B - r_first) : -1;
@@ -561,13 +611,38 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       const StepDesc& d = ctrl->desc[sd];
       const int kind = d.kind;
       if (kind == kEnd) break;
-      const int sb = t & 1;
-      mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
+      const int sb = t & 1;  // S buffer (split) / P buffer
+      if (kSepP<kSplit>) {
+        mbar_wait(&ctrl->s_full[0], t & 1);
+      } else {
+        mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
+      }
       tc_fence_after();
       if (tr0) trace1(1, t, 2);
-      uint32_t x[kBox];
-      tmem_ld32x32b_x64(tmem + lane_off + sb * kBox, x);
+      if (SPF_EXPT == 2 || SPF_EXPT == 6) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
+        if (kSepP<kSplit> && lane == 0) mbar_arrive(&ctrl->s_free[0]);
+        l_run = 1.f;
+        tc_fence_before();
+        mbar_arrive(&ctrl->p_full[sb]);
+        continue;
+      }
+      const uint32_t s_col = kSepP<kSplit> ? 0u : (uint32_t)(sb * kBox);
+      uint32_t x[kCols];                          // own keys c0 .. c0+kCols-1
+      uint32_t y[kHalves > 1 ? kBox - kCols : 1];  // the other half (max only)
+      if (kHalves == 1) {
+        tmem_ld32x32b_x64(tmem + lane_off + s_col, x);
+      } else {
+        tmem_ld32x32b_x32(tmem + lane_off + s_col + c0, x);
+        tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
+      }
       tmem_wait_ld();
+      if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->s_free[0]);
+      }
 
       // valid key slots for this row: a contiguous range [lo, hi)
       int lo = 0, hi = 0;
@@ -586,19 +661,53 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+      if (!__any_sync(0xffffffffu, hi > lo)) {
+        // none of this warp's rows sees the step (the other row block's tile of a union
+        // step, a block-sparse block of the other row): P = 0, softmax state unchanged
+        uint32_t z[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = 0u;
+        if (kSepP<kSplit>) {
+          const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
+          if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, z);
+          else tmem_st32x32b_x32(tmem + lane_off + pcol, z);
+        } else {
+          tmem_st32x32b_x32(tmem + lane_off + sb * kBox, z);
+          if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, z);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&ctrl->p_full[sb]);
+        continue;
+      }
       // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
       if (!(lo == 0 && hi == kBox)) {
+        const int xl = lo - c0, xh = hi - c0;
 #pragma unroll
-        for (int j = 0; j < kBox; ++j) x[j] = (j >= lo && j < hi) ? x[j] : 0xff800000u;
+        for (int j = 0; j < kCols; ++j) x[j] = (j >= xl && j < xh) ? x[j] : 0xff800000u;
+        if (kHalves > 1) {
+          const int yl = lo - (c0 ^ kCols), yh = hi - (c0 ^ kCols);
+#pragma unroll
+          for (int j = 0; j < kBox - kCols; ++j) y[j] = (j >= yl && j < yh) ? y[j] : 0xff800000u;
+        }
       }
-      // row max: four independent 3-input max chains (FMNMX3)
+      // row max over all 64 keys: four independent 3-input max chains (FMNMX3)
       float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < kBox; j += 8) {
+      for (int j = 0; j < kCols; j += 8) {
         mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
         mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
         mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
         mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
+      }
+      if (kHalves > 1) {
+#pragma unroll
+        for (int j = 0; j < kBox - kCols; j += 8) {
+          mx0 = fmax3(mx0, u2f(y[j]), u2f(y[j + 1]));
+          mx1 = fmax3(mx1, u2f(y[j + 2]), u2f(y[j + 3]));
+          mx2 = fmax3(mx2, u2f(y[j + 4]), u2f(y[j + 5]));
+          mx3 = fmax3(mx3, u2f(y[j + 6]), u2f(y[j + 7]));
+        }
       }
       const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
       float alpha = 1.f;
@@ -613,25 +722,20 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
           rescale = true;
         }
       }
-      uint32_t ph[kBox / 2];
-      uint32_t pl[kSplit ? kBox / 2 : 1];
+      uint32_t ph[kCols / 2];
+      uint32_t pl[kSplit ? kCols / 2 : 1];
       // p = 2^(x*c - m): packed FFMA2, MUFU ex2, packed FADD2 row sums
       const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
       const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
       const uint64_t m2 = pack_f32x2(neg_m, neg_m);
       uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
 #pragma unroll
-      for (int j = 0; j < kBox; j += 2) {
-        const uint64_t y = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
-        float p0, p1;
-        if (!kSplit && kEmu1 > 0 && ((j >> 1) % (kEmu1 > 0 ? kEmu1 : 1)) == kEmu1 - 1) {
-          unpack_f32x2(exp2_poly_x2(y), p0, p1);  // part of the exponentials on the FMA pipe
-        } else {
-          float y0, y1;
-          unpack_f32x2(y, y0, y1);
-          p0 = ex2_approx(y0);
-          p1 = ex2_approx(y1);
-        }
+      for (int j = 0; j < kCols; j += 2) {
+        const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
+        float y0, y1;
+        unpack_f32x2(yv, y0, y1);
+        const float p0 = ex2_approx(y0);
+        const float p1 = ex2_approx(y1);
         const uint64_t pp = pack_f32x2(p0, p1);
         switch ((j >> 1) & 3) {
           case 0: s0 = fadd2(s0, pp); break;
@@ -652,31 +756,32 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       l_run = l_run * alpha + sum;
 
       // O rescale needs PV(t-1) retired.  S(t) being ready implies PV(t-2) retired (QK(t)
-      // waited s_free), so pv_done has completed t-1 or t phases: the parity wait for
-      // phase t-1 cannot alias.  tcgen05.ld/st are warp-collective: decide per warp.
-#ifndef SPF_PV_WAIT_EVERY_STEP
-#define SPF_PV_WAIT_EVERY_STEP 0
-#endif
-      if (SPF_PV_WAIT_EVERY_STEP && t > 0) {
-        mbar_wait(&ctrl->pv_done, (t - 1) & 1);
-        tc_fence_after();
-      }
+      // is issued after PV(t-2) and the commit behind s_full tracks every earlier MMA of
+      // the issuing thread), so pv_done has completed t-1 or t phases: the parity wait for
+      // phase t-1 cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
+      // tcgen05.ld/st are warp-collective: decide per warp.
       if (t > 0 && __any_sync(0xffffffffu, rescale)) {
         mbar_wait(&ctrl->pv_done, (t - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < kD; c += 32) {
+        for (int c = 0; c < kOCols; c += 32) {
           uint32_t o[32];
-          tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
+          tmem_ld32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-          tmem_st32x32b_x32(tmem + lane_off + 128 + c, o);
+          tmem_st32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
         }
       }
-      // P(t) -> TMEM over S(t): bf16 pairs, K-major (PV reads A from TMEM)
-      tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
-      if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
+      if (kSepP<kSplit>) {
+        const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
+        if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);
+        else tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
+      } else {
+        tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
+        if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full[sb]);
@@ -687,36 +792,51 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
       mbar_wait(&ctrl->o_ready, 0);
       tc_fence_after();
     }
+    float l_tot = l_run;
+    if (kHalves > 1) {
+      // sum the halves' l through TMEM columns 0..1 (S is dead once every PV retired)
+      uint32_t lv = __float_as_uint(l_run);
+      tmem_st32x32b_x1(tmem + lane_off + half, &lv);
+      tmem_wait_st();
+      tc_fence_before();
+      named_bar_sync(1, 32 * 4 * kHalves);
+      tc_fence_after();
+      uint32_t l2[2];
+      tmem_ld32x32b_x2(tmem + lane_off, l2);
+      tmem_wait_ld();
+      l_tot = u2f(l2[0]) + u2f(l2[1]);
+    }
     {
-      const float inv = (t > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+      const float inv = (t > 0 && l_tot > 0.f) ? 1.f / l_tot : 0.f;
       const int dout = p.d_out;
-      const int64_t obase = ((int64_t)h * S + min(q, S - 1)) * dout;
+      const int64_t obase = ((int64_t)h * S + min(q, S - 1)) * dout + oc0;
+      const int dmine = min(kOCols, dout - oc0);  // columns of this half that exist in the output
 #pragma unroll
-      for (int c = 0; c < kD; c += 32) {
+      for (int c = 0; c < kOCols; c += 32) {
         uint32_t o[32];
         __syncwarp();
         if (t > 0) {  // warp-uniform: every lane loads, only rows < S store
-          tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
+          tmem_ld32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
           tmem_wait_ld();
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] = 0u;
         }
-        if (q >= S) {
+        if (q >= S || dmine <= 0) {
         } else if (p.out_f32) {
           float* out = reinterpret_cast<float*>(p.out) + obase;
-          if (dout == kD) {
+          if (dmine == kOCols) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
               *reinterpret_cast<float4*>(out + c + j) =
                   make_float4(u2f(o[j]) * inv, u2f(o[j + 1]) * inv, u2f(o[j + 2]) * inv, u2f(o[j + 3]) * inv);
           } else {
             for (int j = 0; j < 32; ++j)
-              if (c + j < dout) out[c + j] = u2f(o[j]) * inv;
+              if (c + j < dmine) out[c + j] = u2f(o[j]) * inv;
           }
         } else {
           __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + obase;
-          if (dout == kD) {
+          if (dmine == kOCols) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
               int4 w;
@@ -728,13 +848,12 @@ __global__ void __launch_bounds__(kThreads, kSplit ? 1 : 2)
             }
           } else {
             for (int j = 0; j < 32; ++j)
-              if (c + j < dout) out[c + j] = __float2bfloat16_rn(u2f(o[j]) * inv);
+              if (c + j < dmine) out[c + j] = __float2bfloat16_rn(u2f(o[j]) * inv);
           }
         }
       }
     }
   }
-
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -773,7 +892,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
   if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
   const float scale_log2 = a.scale * 1.4426950408889634f;
   note_launches(1);
-  kern<<<(unsigned)grid, kThreads, L::kSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
+  kern<<<(unsigned)grid, kThreadsT<kSplit>, L::kSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
   return check_cuda(cudaGetLastError(), "sparse_attn_fwd launch");
 }
 

@@ -64,6 +64,16 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
                           int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                           const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
                           void* out, void* workspace, size_t workspace_bytes, void* stream);
+/* Same, and (lse_out != NULL) the per-row log-sum-exp of the cells the layout
+ * covers: lse_out[h][i] = ln sum_{j in cells(i)} exp(scale * q_i.k_j), -inf for a
+ * row with no cell (fp32 [n_q_heads][seq_len]).  With a dense causal layout this is
+ * the softmax normaliser, so exp(lse_sparse - lse_dense) is the attention mass the
+ * layout keeps: the streaming form of attention_ref.attention_recall
+ * (attention_ref.py:128-139) without the S x S probability matrix. */
+int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
+                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
+                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
+                              void* out, float* lse_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Heads selection: the estimation and layout entry points below work on a
  * subset of q-heads given by `head_ids` (device int32 [n_heads]; NULL means

@@ -17,6 +17,17 @@ from .estimator import (
     estimate_vertical_slash_gpu,
 )
 from .kernels import BACKEND, available_backends, sparse_flash_attention, sparse_flash_attention_gpu
+from .metrics import (
+    RunReport,
+    attention_recall_gpu,
+    dense_layout,
+    kernel_sparsity,
+    modeled_kernel_sparsity,
+    report_head,
+    report_layer,
+    reports_to_csv,
+    reports_to_json,
+)
 from .patterns import (
     AShape,
     BlockSparse,
@@ -33,6 +44,15 @@ from .patterns import (
     save_pattern_configs,
 )
 from .prefill import LayerLayout, build_layer_layout, sparse_prefill_attention
+from .search import (
+    SearchCandidate,
+    SearchResult,
+    calibrate_candidate,
+    calibrate_search_space,
+    candidate_errors_gpu,
+    default_budget,
+    search_optimal_pattern,
+)
 from .sparse_attn import (
     AttentionInputs,
     block_indices_to_layout,
@@ -44,8 +64,3 @@ from .sparse_attn import (
 from .vs_index import build_vs_layout, build_vs_layout_with_stats
 
 __version__ = "0.1.0"
-
-
-def kernel_sparsity(layout: SparseLayout) -> float:
-    """metrics.py:43-45: fraction of causal cells NOT computed."""
-    return 1.0 - layout_area(layout) / causal_area(layout.seq_len)

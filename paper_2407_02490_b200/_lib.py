@@ -32,6 +32,8 @@ SIGNATURES = {
     "spf_sparse_flash_workspace_size": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "spf_sparse_flash_rows": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
                                        _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+    "spf_sparse_flash_rows_lse": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
+                                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "spf_vs_estimate_workspace_size": (_c_size, [_c_int] * 8),
     "spf_vs_estimate": (_c_int, [_c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
                                  _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),

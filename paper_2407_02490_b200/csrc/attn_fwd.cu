@@ -806,6 +806,8 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       tmem_wait_ld();
       l_tot = u2f(l2[0]) + u2f(l2[1]);
     }
+    if (p.lse != nullptr && half == 0 && q < S)
+      p.lse[(int64_t)h * S + q] = (t > 0 && l_tot > 0.f) ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
     {
       const float inv = (t > 0 && l_tot > 0.f) ? 1.f / l_tot : 0.f;
       const int dout = p.d_out;
@@ -911,7 +913,7 @@ int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream) {
     const char* e = getenv("SPF_ATTN_KERNEL");
     return e ? atoi(e) : 1;
   }();
-  if (kernel_choice == 2 && attn2_supported(a)) return launch_sparse_attn2(a, stream);
+  if (kernel_choice == 2 && a.lse == nullptr && attn2_supported(a)) return launch_sparse_attn2(a, stream);
   if (a.kD == 128) return a.split ? launch_impl<128, true>(a, stream) : launch_impl<128, false>(a, stream);
   if (a.kD == 64) return a.split ? launch_impl<64, true>(a, stream) : launch_impl<64, false>(a, stream);
   return set_error(2, "padded head_dim must be 64 or 128 (got %d)", a.kD);

@@ -119,6 +119,15 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
                           int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                           const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
                           void* out, void* workspace, size_t workspace_bytes, void* stream) {
+  return spf_sparse_flash_rows_lse(dtype, q, k, v, n_q_heads, n_kv_heads, seq_len, head_dim, scale, block_size,
+                                   tile_starts, tile_offsets, col_indices, col_offsets, out, nullptr, workspace,
+                                   workspace_bytes, stream);
+}
+
+int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
+                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
+                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
+                              void* out, float* lse_out, void* workspace, size_t workspace_bytes, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype != SPF_DTYPE_BF16 && dtype != SPF_DTYPE_F32) return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
   if (seq_len < 1 || head_dim < 1 || n_q_heads < 1 || n_kv_heads < 1)
@@ -147,6 +156,7 @@ int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v
   a.split = split;
   a.work_order = nullptr;
   a.n_work = 0;
+  a.lse = lse_out;
   const size_t need = spf_sparse_flash_workspace_size(dtype, n_q_heads, n_kv_heads, seq_len, head_dim);
   if (need == 0) {
     a.q_hi = q;

@@ -33,6 +33,7 @@ struct AttnArgs {
   bool split;
   const int32_t* work_order;  // optional: CTA -> work-item list (nullptr = all items, heavy rows first)
   int n_work;                 // number of entries in work_order
+  float* lse;                 // optional [Hq][S]: natural-log sum of exp(scale * q.k) over the row's cells
 };
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);

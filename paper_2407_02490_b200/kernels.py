@@ -41,12 +41,14 @@ def _flatten(per_row, n_rows: int):
 def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float, block_size: int,
                                tile_starts: torch.Tensor, tile_offsets: torch.Tensor, col_indices: torch.Tensor,
                                col_offsets: torch.Tensor, out: torch.Tensor | None = None,
-                               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                               stream: torch.cuda.Stream | None = None,
+                               lse: torch.Tensor | None = None) -> torch.Tensor:
     """Batched sparse FlashAttention on device tensors.
 
     q [Hq, S, d], k/v [Hkv, S, d] (bf16 or fp32, contiguous, same dtype);
     CSR over (head, row): offsets int64 [Hq*n_rows+1], entries int32.
-    Returns out [Hq, S, d] in the input dtype.
+    Returns out [Hq, S, d] in the input dtype.  ``lse`` (optional fp32 [Hq, S])
+    receives each row's natural-log sum of exp(scale * q.k) over its cells.
     """
     dev = _dev.require_cuda(q.device)
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
@@ -69,10 +71,12 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     ws = _dev.workspace(ws_bytes, dev)
     ts = tile_starts if tile_starts.numel() else None
     cs = col_indices if col_indices.numel() else None
-    _lib.check(lib.spf_sparse_flash_rows(
+    if lse is not None and (lse.dtype != torch.float32 or lse.numel() != hq * s_len or not lse.is_contiguous()):
+        raise ValueError("lse must be a contiguous fp32 [Hq, S] tensor")
+    _lib.check(lib.spf_sparse_flash_rows_lse(
         dtype, _dev.ptr(q), _dev.ptr(k), _dev.ptr(v), hq, hkv, s_len, d, float(scale), int(block_size),
-        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(out),
-        _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows")
+        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(out), _dev.ptr(lse),
+        _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows_lse")
     return out
 
 

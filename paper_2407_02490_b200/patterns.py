@@ -235,7 +235,18 @@ def _model_area(cfg: HeadPatternConfig, seq_len: int, block_size: int) -> int:
     """patterns.py:221-233 (A-shape: realized layout; BS: exact; VS: model)."""
     b = block_size
     if isinstance(cfg, AShape):
-        return layout_area(a_shape_layout(seq_len, cfg, b))
+        # area of the realized layout (patterns.py:109-128), closed form per row: the
+        # aligned sink tiles [0, a) and window tiles [w0, r] are all below the diagonal
+        # except tile r (the triangle), so no layout needs to be built for the model
+        n = n_block_rows(seq_len, b)
+        r = np.arange(n, dtype=np.int64)
+        q_start = r * b
+        q_end = np.minimum(q_start + b, seq_len)
+        h = q_end - q_start
+        a = (np.minimum(cfg.global_tokens, q_end) + b - 1) // b
+        w0 = np.maximum(0, q_start - cfg.local_window) // b
+        n_tiles = (r + 1 - w0) + np.minimum(a, w0)
+        return int(np.sum((n_tiles - 1) * h * b + h * (h + 1) // 2))
     if isinstance(cfg, BlockSparse):
         b = cfg.block_size
         n = n_block_rows(seq_len, b)

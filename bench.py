@@ -204,6 +204,9 @@ def main():
     q0 = shard.q_begin
     all_cfgs = layer_configs(cfg)[:L]
     cfgs = [row[q0:q0 + hq_loc] for row in all_cfgs]
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    table = PatternTable(cfgs)  # this rank's heads; device head groups cached per layer
     gen = g_local_qkv if cfg["inputs"] == "G-local" else g_iid_qkv
 
     # ---- inputs resident in HBM (per layer; this rank's kv groups) ----
@@ -223,7 +226,7 @@ def main():
 
     def step(record=False):
         for layer in range(L):
-            lay = P.build_layer_layout(Q[layer], K[layer], cfgs[layer], B)
+            lay = P.build_layer_layout(Q[layer], K[layer], cfgs[layer], B, groups=table.device_groups(layer, dev))
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -302,7 +305,7 @@ def main():
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, P, torch, Q, K, V, cfgs, B, L, stream)
+        e2e = run_e2e(args, SparsePrefill(table, B), torch, Q, K, V, L, stream)
         e2e["value"] = round(max_over_ranks(e2e["value"], device=dev), 3)
 
     # ---- dense FlashAttention-class baseline (torch SDPA, bf16, causal, GQA), one layer ----
@@ -345,10 +348,11 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(args, P, torch, Q, K, V, cfgs, B, L, stream):
+def run_e2e(args, model, torch, Q, K, V, L, stream):
     """Public API with host buffers: per layer, H2D of Q/K/V from pinned host
-    memory (copy stream, prefetching layer l+1 during layer l), the layer
-    pipeline, and D2H of the output into pinned host memory."""
+    memory (copy stream, prefetching layer l+1 during layer l), the model
+    driver's layer (driver.SparsePrefill: estimation, compaction, attention),
+    and D2H of the output into pinned host memory."""
     dev = Q[0].device
     slots = 2
     host_q = [Q[i % L].cpu().pin_memory() for i in range(slots)]
@@ -385,7 +389,7 @@ def run_e2e(args, P, torch, Q, K, V, cfgs, B, L, stream):
             if layer + 1 < L:
                 issue_h2d(layer + 1)
             comp.wait_event(ready[slot])
-            P.sparse_prefill_attention(dq[slot], dk[slot], dv[slot], cfgs[layer], B, out=do[slot])
+            model.layer(layer, dq[slot], dk[slot], dv[slot], out=do[slot])
             ev = torch.cuda.Event()
             ev.record(comp)
             with torch.cuda.stream(d2h):
@@ -412,7 +416,7 @@ def run_e2e(args, P, torch, Q, K, V, cfgs, B, L, stream):
     d2h_bytes = L * Q[0].numel() * 2
     return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d_bytes),
             "d2h_bytes_per_step": int(d2h_bytes), "steps": n,
-            "note": "public API sparse_prefill_attention per layer; pinned host buffers (2-slot ring of layer "
+            "note": "public API driver.SparsePrefill.layer per layer; pinned host buffers (2-slot ring of layer "
                     "inputs), H2D prefetch of layer l+1 overlapping layer l, D2H of every layer's output"}
 
 

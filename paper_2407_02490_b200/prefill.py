@@ -78,8 +78,11 @@ def _group_heads(head_cfgs, device):
 
 
 def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: int = 64,
-                       stream=None) -> LayerLayout:
-    """Estimation + index compaction for every head of a layer (steps 1-2)."""
+                       stream=None, groups=None) -> LayerLayout:
+    """Estimation + index compaction for every head of a layer (steps 1-2).
+
+    ``groups`` may pass the layer's precomputed device head groups
+    (driver.PatternTable.device_groups) instead of regrouping ``head_cfgs``."""
     dev = _dev.require_cuda(q.device)
     hq, s_len, _ = q.shape
     if len(head_cfgs) != hq:
@@ -89,7 +92,8 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
             raise ValueError("all heads of a layer must share one block size "
                              f"(BlockSparse block_size {cfg.block_size} != {block_size})")
     n = n_block_rows(s_len, block_size)
-    groups = _group_heads(head_cfgs, dev)
+    if groups is None:
+        groups = _group_heads(head_cfgs, dev)
     tc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
     cc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
     vs_sel = {}
@@ -121,9 +125,9 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
 
 def sparse_prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, head_cfgs, block_size: int = 64,
                              scale: float | None = None, out: torch.Tensor | None = None, stream=None,
-                             return_layout: bool = False):
+                             return_layout: bool = False, groups=None):
     """Full layer: q [Hq, S, d], k/v [Hkv, S, d] (bf16) -> out [Hq, S, d]."""
-    layout = build_layer_layout(q, k, head_cfgs, block_size, stream)
+    layout = build_layer_layout(q, k, head_cfgs, block_size, stream, groups)
     d = q.shape[-1]
     sc = 1.0 / math.sqrt(d) if scale is None else float(scale)
     out = kernels.sparse_flash_attention_gpu(q, k, v, sc, block_size, layout.tiles, layout.tile_offsets,

@@ -1,0 +1,74 @@
+"""Pattern-table model driver: config JSON v1 validation on the
+host, and on the GPU equality with the per-layer pipeline it wraps."""
+
+import json
+import os
+
+import pytest
+
+from conftest import REPO
+
+C2 = os.path.join(REPO, "configs", "llama3_8b_1m_c2.json")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2407_02490_b200 as P
+
+    return P
+
+
+def test_c2_table_loads_and_round_trips(P, tmp_path):
+    from paper_2407_02490_b200.driver import PatternTable
+
+    t = PatternTable.load(C2)
+    assert (t.n_layers, t.n_heads) == (32, 32)
+    counts = t.pattern_counts()
+    assert counts["VerticalSlash"] > 0.9 * 32 * 32 and counts["AShape"] > 0 and counts["BlockSparse"] > 0
+    p = tmp_path / "t.json"
+    t.save(p)
+    t2 = PatternTable.load(p)
+    assert t2.layers == t.layers
+    assert json.loads(p.read_text())["format_version"] == 1
+    assert len(t.modeled_flops(131072, 128)) == 32
+
+
+def test_table_validation(P):
+    from paper_2407_02490_b200.driver import PatternTable
+    from paper_2407_02490_b200.patterns import config_to_entry
+
+    e = [config_to_entry(l, h, P.VerticalSlash(10, 20)) for l in range(2) for h in range(3)]
+    assert PatternTable.from_entries(e).n_heads == 3
+    with pytest.raises(ValueError, match="missing"):
+        PatternTable.from_entries(e[:-1])
+    with pytest.raises(ValueError, match="duplicate"):
+        PatternTable.from_entries(e + [e[0]])
+    with pytest.raises(ValueError, match="unknown pattern name"):
+        PatternTable.from_entries([{"layer": 0, "head": 0, "pattern": "dense", "params": {}}])
+    with pytest.raises(ValueError, match="block sizes"):
+        PatternTable([[P.BlockSparse(4, 32), P.BlockSparse(4, 64)]])
+    with pytest.raises(TypeError):
+        PatternTable([[object()]])
+    t = PatternTable([[P.BlockSparse(4, 32), P.AShape(1, 2)], [P.AShape(1, 2), P.VerticalSlash(1, 1)]])
+    assert t.block_size(0) == 32 and t.block_size(1) == 64
+
+
+@pytest.mark.gpu
+def test_driver_matches_layer_pipeline(P):
+    import torch
+
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(3)
+    hq, hkv, s, d = 8, 2, 2048, 128
+    table = PatternTable([[P.VerticalSlash(64, 256)] * 5 + [P.AShape(64, 512), P.BlockSparse(8), P.VerticalSlash(16, 64)],
+                          [P.AShape(128, 256)] * 4 + [P.VerticalSlash(100, 300)] * 4])
+    layers = [tuple(torch.randn(h, s, d, generator=g, device=dev).to(torch.bfloat16) for h in (hq, hkv, hkv))
+              for _ in range(2)]
+    outs = list(SparsePrefill(table)(layers))
+    for l, (q, k, v) in enumerate(layers):
+        want = P.sparse_prefill_attention(q, k, v, table.layer(l), 64)
+        assert torch.equal(outs[l], want)
+    with pytest.raises(ValueError):
+        SparsePrefill(table).layer(0, layers[0][0][:4].contiguous(), layers[0][1], layers[0][2])

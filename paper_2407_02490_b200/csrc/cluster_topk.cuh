@@ -27,6 +27,9 @@ struct ClusterTopK {
   static constexpr int kBins = 1 << kBits;
   static constexpr int kPer = kBins / kThreads;
   static constexpr int kU = 8;  // loads in flight per thread
+  // Once a CTA's share of the boundary bucket fits here, its remaining radix rounds
+  // histogram this list instead of re-reading the whole slice.
+  static constexpr int kCap = 2048;
   using Scan = cub::BlockScan<int, kThreads>;
 
   struct Storage {
@@ -38,6 +41,8 @@ struct ClusterTopK {
     int cnt[2][kCl];    // exchanged per-CTA counts (T-valued, selected)
     double lo[kCl], hi[kCl];
     int eq[kCl];
+    int ncand;
+    uint64_t cand[kCap];  // keys of this CTA's slice inside the current boundary bucket
   };
 
   // Aggregated increment: lanes whose digit equals lane-leader's digit add once.
@@ -69,13 +74,21 @@ struct ClusterTopK {
     uint64_t prefix = 0, pmask = 0;
     int krem = k;
     int round = 0;
+    int ncand = -1;  // >= 0: the slice's boundary-bucket keys are in sm.cand[0, ncand)
     for (int shift = 64 - kBits; shift > -kBits; shift -= kBits, ++round) {
       const int sh = shift < 0 ? 0 : shift;
       const int width = shift < 0 ? kBits + shift : kBits;
       const uint64_t dmask = (uint64_t)((1u << width) - 1);
       for (int b = tid; b < kBins; b += kThreads) sm.hist[b] = 0;
       __syncthreads();
-      for (int base = s0; base < s1; base += kThreads * kU) {
+      if (ncand >= 0) {
+        for (int i0 = 0; i0 < ncand; i0 += kThreads) {  // warp-uniform trip count
+          const int i = i0 + tid;
+          const uint64_t key = i < ncand ? sm.cand[i] : 0ull;
+          hist_add(sm.hist, i < ncand && (key & pmask) == prefix, (int)((key >> sh) & dmask));
+        }
+      }
+      for (int base = ncand >= 0 ? s1 : s0; base < s1; base += kThreads * kU) {
         double v[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {  // kU independent loads in flight per thread
@@ -128,6 +141,38 @@ struct ClusterTopK {
       prefix = sm.prefix;
       krem = sm.krem;
       pmask |= dmask << sh;
+      if (ncand < 0 && shift > 0) {
+        const int mine = sm.hist[(int)((prefix >> sh) & dmask)];  // this CTA's keys in the new bucket
+        __syncthreads();
+        if (mine <= kCap) {  // one more pass over the slice, then lists only
+          if (tid == 0) sm.ncand = 0;
+          __syncthreads();
+          for (int base = s0; base < s1; base += kThreads * kU) {
+            double v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int i = base + u * kThreads + tid;
+              v[u] = i < s1 ? vals[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int i = base + u * kThreads + tid;
+              const uint64_t key = mono_key(v[u]);
+              const bool hit = i < s1 && (key & pmask) == prefix;
+              const unsigned m = __ballot_sync(0xffffffffu, hit);
+              if (m) {
+                const int lane = tid & 31;
+                int at = 0;
+                if (lane == __ffs(m) - 1) at = atomicAdd(&sm.ncand, __popc(m));
+                at = __shfl_sync(0xffffffffu, at, __ffs(m) - 1);
+                if (hit) sm.cand[at + __popc(m & ((1u << lane) - 1))] = key;
+              }
+            }
+          }
+          __syncthreads();
+          ncand = sm.ncand;
+        }
+      }
     }
     const uint64_t thr = prefix;
     const uint64_t key0 = mono_key(vals[0]);
@@ -137,7 +182,7 @@ struct ClusterTopK {
     // per-thread contiguous sub-slices, index order
     const int per = (s1 - s0 + kThreads - 1) / kThreads;
     const int b0 = min(s1, s0 + tid * per), b1 = min(s1, b0 + per);
-    int eq = 0;
+    int eq = 0, gt = 0;
     double below = -INFINITY, above = INFINITY;
     for (int i0 = b0; i0 < b1; i0 += kU) {
       double v[kU];
@@ -149,7 +194,10 @@ struct ClusterTopK {
         const uint64_t key = mono_key(v[u]);
         if (key == thr) ++eq;
         else if (key < thr) below = fmax(below, v[u]);
-        else above = fmin(above, v[u]);
+        else {
+          above = fmin(above, v[u]);
+          ++gt;
+        }
       }
     }
     int eq_base, eq_cta;
@@ -198,24 +246,9 @@ struct ClusterTopK {
     }
     int eq_glob = 0;
     for (int r = 0; r < rank; ++r) eq_glob += sm.cnt[0][r];
-    // selected count
-    int sel = 0;
-    {
-      int r = eq_glob + eq_base;
-      for (int i0 = b0; i0 < b1; i0 += kU) {
-        double v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) v[u] = i0 + u < b1 ? vals[i0 + u] : -INFINITY;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          if (i0 + u >= b1) break;
-          const uint64_t key = mono_key(v[u]);
-          const bool is_eq = key == thr;
-          sel += ((key > thr) || (is_eq && r < quota)) ? 1 : 0;
-          r += is_eq;
-        }
-      }
-    }
+    // selected count: every key above the threshold, plus this thread's T-valued keys
+    // whose global rank among the T-valued ones (index order) is below the quota
+    const int sel = gt + min(eq, max(0, quota - (eq_glob + eq_base)));
     int sel_base, sel_cta;
     Scan(sm.scan).ExclusiveSum(sel, sel_base, sel_cta);
     if (tid < kCl) *cl.map_shared_rank(&sm.cnt[1][rank], tid) = sel_cta;

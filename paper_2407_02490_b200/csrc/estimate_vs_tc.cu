@@ -63,7 +63,14 @@ struct TcArgs {
   // for the exact fallback's tile skipping
   float* tile_max;   // [n_heads][64][n_tiles] raw row max per 128-key tile
   float* row_mc;     // [n_heads][64] mc per slot
+  uint8_t* live;     // [groups][n_tiles] pass-2 tile holds a probability that is not flushed to 0
 };
+
+// A tile whose largest exponent y = fma(x_max, c, -mc) is below kDeadExp contributes exactly
+// nothing: ex2.approx.ftz flushes 2^y < 2^-126 to +0.  One unit of margin covers the last-bit
+// difference between the pass-1 and pass-2 accumulation orders of the same dot product.
+constexpr float kDeadExp = -127.f;
+constexpr int kMaxList = 2048;  // live-tile list capacity per pass-2 CTA (more tiles: no skipping)
 
 struct TcCtrl {
   uint64_t q_full;
@@ -73,6 +80,7 @@ struct TcCtrl {
   uint64_t acc_empty[2];
   uint32_t tmem_base;
   int nh;
+  int n_list;
   int slot[kMaxMembers];
   int head[kMaxMembers];
 };
@@ -88,7 +96,8 @@ struct TcLayout {
   static constexpr int kOffRow = kOffK + kStages * kStageBytes;      // pass 2: float2 (m, il) [256]
   static constexpr int kOffDiag = kOffRow + kGroupRows * 8;          // pass 2: float [2][4 members][4 wk][3][32]
   static constexpr int kDiagBytes = 2 * kMaxMembers * 4 * 3 * 32 * 4;
-  static constexpr int kOffCtrl = kOffDiag + kDiagBytes;
+  static constexpr int kOffList = kOffDiag + kDiagBytes;             // pass 2: live tile list
+  static constexpr int kOffCtrl = kOffList + kMaxList * 4;
   static constexpr int kSmem = kOffCtrl + (int)sizeof(TcCtrl);
 };
 
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   const int nh = ctrl->nh;
-  if (nh == 0 || t_begin >= t_end) return;  // CTA-uniform, before TMEM allocation
+  if (nh == 0 || chunk >= a.n_tiles) return;  // CTA-uniform, before TMEM allocation
   if (kPass == 2) {
     // row stats per member pair and tail row: {-mc(2p), -mc(2p+1), 1/l(2p), 1/l(2p+1)}
     float4* rs = reinterpret_cast<float4*>(smem + L::kOffRow);
@@ -159,7 +168,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = ctrl->tmem_base;
-  const int n_tiles_cta = t_end - t_begin;
+  // Pass 1: chunk c takes tiles T-1-c, T-1-c-n_chunks, ... (interleaved, highest first), so
+  // every chunk meets the diagonal region first, sets its running row max early and skips
+  // the exponentials of the tiles that flush to zero -- balanced across chunks.  Pass 2: the
+  // group's live tiles (a.live) are split evenly over its chunks.
+  int n_tiles_cta = kPass == 1 ? (chunk < a.n_tiles ? (a.n_tiles - chunk + a.n_chunks - 1) / a.n_chunks : 0)
+                               : t_end - t_begin;
+  int* s_list = reinterpret_cast<int*>(smem + L::kOffList);
+  bool use_list = false;
+  if (kPass == 2) {
+    if (warp == 0) {
+      const uint8_t* lv_g = a.live + (int64_t)gy * a.n_tiles;
+      int nl = 0;
+      for (int b = 0; b < a.n_tiles; b += 32) nl += __popc(__ballot_sync(0xffffffffu, b + lane < a.n_tiles && lv_g[b + lane]));
+      const int lo = (int)((int64_t)chunk * nl / a.n_chunks), hi = (int)((int64_t)(chunk + 1) * nl / a.n_chunks);
+      int n = -1;
+      if (hi - lo <= kMaxList) {
+        int rank = 0;
+        n = 0;
+        for (int b = 0; b < a.n_tiles && rank < hi; b += 32) {
+          const int t = b + lane;
+          const bool lv = t < a.n_tiles && lv_g[t];
+          const unsigned m = __ballot_sync(0xffffffffu, lv);
+          const int r = rank + __popc(m & ((1u << lane) - 1));
+          if (lv && r >= lo && r < hi) s_list[r - lo] = t;
+          rank += __popc(m);
+        }
+        n = hi - lo;
+      }
+      if (lane == 0) ctrl->n_list = n;
+    }
+    __syncthreads();
+    if (ctrl->n_list >= 0) {
+      use_list = true;
+      n_tiles_cta = ctrl->n_list;
+    }
+  }
+  auto tile_of = [&](int t) {
+    return kPass == 1 ? a.n_tiles - 1 - (chunk + t * a.n_chunks) : (use_list ? s_list[t] : t_begin + t);
+  };
 
   if (warp == 0) {
     // =============================== TMA producer ===============================
@@ -177,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&ctrl->k_full[st], (uint32_t)L::kStageBytes);
         uint8_t* kst = smem + L::kOffK + st * L::kStageBytes;
         for (int at = 0; at < L::kAtoms; ++at)
-          tma_load_3d(kst + at * L::kKAtom, &tm_k, &ctrl->k_full[st], at * 64, (t_begin + t) * kKeys, kvh);
+          tma_load_3d(kst + at * L::kKAtom, &tm_k, &ctrl->k_full[st], at * 64, tile_of(t) * kKeys, kvh);
       }
     }
     __syncwarp();
@@ -244,7 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       double l_run = 0.0;
       for (int t = 0; t < n_tiles_cta; ++t) {
         const int buf = t & 1;
-        const int tile0 = (t_begin + t) * kKeys;
+        const int tile = tile_of(t);
+        const int tile0 = tile * kKeys;
         mbar_wait(&ctrl->acc_full[buf], (t >> 1) & 1);
         tc_fence_after();
         if (active) {
@@ -276,7 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[j] = ok ? x[j] : 0xf149f2cau;  // -1e30 (finite): 2^(y) underflows to 0
             }
           }
-          a.tile_max[((int64_t)ctrl->slot[mm] * kTailRows + i) * a.n_tiles + t_begin + t] = tmax;
+          a.tile_max[((int64_t)ctrl->slot[mm] * kTailRows + i) * a.n_tiles + tile] = tmax;
+          // every exponent of this row below the flush threshold: the tile adds exactly 0
+          const bool dead = n_valid <= 0 || (m_run != -INFINITY && tmax <= m_run && fmaf(tmax, c, -mc_run) < kDeadExp);
+          const bool warp_dead = __all_sync(0xffffffffu, dead);
           if (n_valid > 0) {
             amax = fmax3(amax, fabsf(tmax), fabsf(tmin));
             if (tmax > m_run) {
@@ -285,19 +336,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               m_run = tmax;
               mc_run = mc_new;
             }
-            const uint64_t nm2 = pack_f32x2(-mc_run, -mc_run);
-            uint64_t s0 = 0, s1 = 0;
+            if (!warp_dead) {
+              const uint64_t nm2 = pack_f32x2(-mc_run, -mc_run);
+              uint64_t s0 = 0, s1 = 0;
 #pragma unroll
-            for (int j = 0; j < kKeys; j += 4) {
-              float y0, y1, y2, y3;
-              unpack_f32x2(ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, nm2), y0, y1);
-              unpack_f32x2(ffma2(pack_f32x2(u2f(x[j + 2]), u2f(x[j + 3])), c2, nm2), y2, y3);
-              s0 = fadd2(s0, pack_f32x2(ex2_approx(y0), ex2_approx(y1)));
-              s1 = fadd2(s1, pack_f32x2(ex2_approx(y2), ex2_approx(y3)));
+              for (int j = 0; j < kKeys; j += 4) {
+                float y0, y1, y2, y3;
+                unpack_f32x2(ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, nm2), y0, y1);
+                unpack_f32x2(ffma2(pack_f32x2(u2f(x[j + 2]), u2f(x[j + 3])), c2, nm2), y2, y3);
+                s0 = fadd2(s0, pack_f32x2(ex2_approx(y0), ex2_approx(y1)));
+                s1 = fadd2(s1, pack_f32x2(ex2_approx(y2), ex2_approx(y3)));
+              }
+              float a0, a1;
+              unpack_f32x2(fadd2(s0, s1), a0, a1);
+              l_run += (double)(a0 + a1);
             }
-            float a0, a1;
-            unpack_f32x2(fadd2(s0, s1), a0, a1);
-            l_run += (double)(a0 + a1);
           }
         } else {
           tc_fence_before();
@@ -320,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t col1 = (uint32_t)((m1 < nh ? m1 : m0) * kTailRows);
       for (int t = 0; t < n_tiles_cta; ++t) {
         const int buf = t & 1;
-        const int tile0 = (t_begin + t) * kKeys;
+        const int tile0 = tile_of(t) * kKeys;
         const int j = tile0 + quarter * 32 + lane;  // this thread's key
         mbar_wait(&ctrl->acc_full[buf], (t >> 1) & 1);
         tc_fence_after();
@@ -447,6 +500,41 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
   }
 }
 
+// Pass-2 tile liveness per group: a tile is live if any member row has an exponent at or
+// above kDeadExp there (tile_max and the final mc from pass 1 / combine).  Dead tiles'
+// vertical scores are written here (zeros); their slash contributions are zero already.
+__global__ void __launch_bounds__(256) vs_tc_live_kernel(const TcArgs a) {
+  // 32 tiles per CTA; the 8 warps split the (member, row) pairs and OR their verdicts
+  __shared__ int slot[kMaxMembers], head[kMaxMembers], nh_s;
+  __shared__ int lv[32];
+  const int gy = blockIdx.y;
+  if (threadIdx.x == 0) nh_s = group_members(a, gy, slot, head);
+  if (threadIdx.x < 32) lv[threadIdx.x] = 0;
+  __syncthreads();
+  const int nh = nh_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  if (t < a.n_tiles) {
+    bool live = false;
+    for (int r = w; r < nh * kTailRows && !live; r += 8) {
+      const int mm = r / kTailRows, i = r % kTailRows;
+      const int64_t row = (int64_t)slot[mm] * kTailRows + i;
+      live = fmaf(a.tile_max[row * a.n_tiles + t], a.c_hi, -a.row_mc[row]) >= kDeadExp;
+    }
+    if (live) lv[lane] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && t < a.n_tiles) a.live[(int64_t)gy * a.n_tiles + t] = (uint8_t)lv[threadIdx.x];
+  for (int u = 0; u < 32; ++u) {  // zero the vertical scores of the dead tiles (coalesced)
+    const int tu = blockIdx.x * 32 + u;
+    if (tu >= a.n_tiles || lv[u]) continue;
+    for (int x = threadIdx.x; x < nh * kKeys; x += 256) {
+      const int mm = x / kKeys, j = tu * kKeys + x % kKeys;
+      if (j < a.S) a.vscore[(int64_t)slot[mm] * a.S + j] = 0.0;
+    }
+  }
+}
+
 // Top-k (estimator.py:59-79) of the fp64 score vectors plus certification of the
 // selected set against the error threshold tau: flag the head when the
 // boundary (k-th vs (k+1)-th, the k-th vs (k-1)-th when index 0 must be forced,
@@ -505,6 +593,7 @@ int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv
   a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   a.tile_max = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * a.n_tiles * 4));
   a.row_mc = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * 4));
+  a.live = take((size_t)n_groups * a.n_tiles);
   int32_t* flags_ws = reinterpret_cast<int32_t*>(take((size_t)n_heads * 4));
 
   CUtensorMap tq, tk;
@@ -527,10 +616,11 @@ int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv
   int32_t* flags = uncertain ? uncertain : flags_ws;
   if (!uncertain && (rc = check_cuda(cudaMemsetAsync(flags, 0, (size_t)n_heads * 4, st), "memset flags"))) return rc;
   const dim3 grid((unsigned)a.n_chunks, (unsigned)n_groups);
-  note_launches(4);  // pass 1, combine, pass 2, top-k
+  note_launches(5);  // pass 1, combine, liveness, pass 2, top-k
   vs_tc_kernel<kD, 1><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
   if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 1"))) return rc;
   vs_tc_combine_kernel<<<n_groups, kGroupRows, 0, st>>>(a);
+  vs_tc_live_kernel<<<dim3((unsigned)((a.n_tiles + 31) / 32), (unsigned)n_groups), 256, 0, st>>>(a);
   vs_tc_kernel<kD, 2><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
   if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 2"))) return rc;
   vs_topk_certify_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
@@ -558,7 +648,8 @@ size_t vs_fast_workspace_size(int n_q_heads, int n_kv_heads, int n_heads, int se
   const size_t part = n_groups * n_chunks * kGroupRows;
   return al(part * 4) + al(part * 8) + al(part * 4) + 2 * al(n_groups * kGroupRows * 4) + al(n_heads * 4) +
          2 * al((size_t)n_heads * seq_len * 8) + al((size_t)n_heads * kTailRows * n_tiles * 4) +
-         al((size_t)n_heads * kTailRows * 4) + al(n_heads * 4) + vs_exact_workspace_size(n_heads, seq_len, kTailRows);
+         al((size_t)n_heads * kTailRows * 4) + al(n_groups * n_tiles) + al(n_heads * 4) +
+         vs_exact_workspace_size(n_heads, seq_len, kTailRows);
 }
 
 int vs_estimate_fast(const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,

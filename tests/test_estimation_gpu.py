@@ -197,3 +197,23 @@ def test_vs_ties_resolved_by_lowest_index(P):
         vert, sl = P.estimate_vertical_slash_gpu(tq, tk, cfg, mode=mode)
         np.testing.assert_array_equal(vert[0].cpu().numpy(), wv, err_msg=mode)
         np.testing.assert_array_equal(sl[0].cpu().numpy(), ws, err_msg=mode)
+
+
+@pytest.mark.parametrize("s", [65536 + 100, 200000])
+def test_vs_fast_dead_tile_skipping_matches_exact(P, s):
+    """Long G-local sequences: most 128-key tiles lie > 2^127 below the row max and are
+    skipped by both tensor-core passes (estimate_vs_tc.cu, kDeadExp); the index sets
+    still equal the fp64 path's and the skipped tiles' vertical scores are exactly 0."""
+    from benchmarks.workloads import g_local_qkv
+
+    from paper_2407_02490_b200.estimator import vs_estimate_async
+
+    q, k, _ = g_local_qkv(8, 2, s, 128, seed=7, device="cuda")
+    cfg = P.VerticalSlash(1000, 6096, 64)
+    ids = torch.tensor([5, 0, 2, 7, 3], dtype=torch.int32, device="cuda")
+    vf, sf, vsf, ssf, _ = vs_estimate_async(q, k, cfg, ids, mode="fast", with_scores=True)
+    ve, se, vse, sse, _ = vs_estimate_async(q, k, cfg, ids, mode="exact", with_scores=True)
+    assert torch.equal(vf, ve) and torch.equal(sf, se)
+    # far-from-diagonal keys: probabilities below fp32's range in both paths
+    far = s // 4
+    assert float(vsf[:, :far].abs().max()) == 0.0 and float(vse[:, :far].abs().max()) == 0.0

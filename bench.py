@@ -134,8 +134,7 @@ def run_reference_arm(args, cfg):
               f"full index build, kernel on {args.ref_rows} sampled row blocks extrapolated by tiles+chips; "
               f"kernel = {'reference _core.pyx (oracle/_ref)' if info['ref_kernel'] else 'oracle port'}; "
               f"step latency = sum(item s)/cores")
-    line = {"impl": "reference", "metric": "pre-fill attention latency (ms), LLaMA-3-8B-1M attention, 32 layers "
-            "mixed per-head patterns @128K", "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_name(args, cfg), "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 3), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 storage)", "data": "synthetic (G-local)",
             "config": {"workload": cfg["workload"], "seq_len": cfg["seq_len"], "layers": cfg["layers"]},
@@ -147,6 +146,12 @@ def run_reference_arm(args, cfg):
 
 
 # ----------------------------------------------------------------------------- helpers
+def metric_name(args, cfg) -> str:
+    if args.config == "c2":
+        return "pre-fill attention latency (ms), LLaMA-3-8B-1M attention, 32 layers mixed per-head patterns @128K"
+    return f"pre-fill attention latency (ms), {cfg['workload']}"
+
+
 def union_steps(tiles_np, toff_np, n_rows, hq):
     """Kernel steps of the 128-row CTAs: |tiles(2p) U tiles(2p+1)| per pair."""
     import numpy as np
@@ -192,10 +197,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for exercising the multi-rank path on a one-GPU box: every rank on GPU 0,
+    # gloo for the barriers / max-reduction (the data path has no collective either way)
+    if os.environ.get("BENCH_SINGLE_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     S, HQ, HKV, L, D, B = cfg["seq_len"], cfg["hq"], cfg["hkv"], cfg["layers"], 128, 64
     from paper_2407_02490_b200.sharding import max_over_ranks, shard_heads
 
@@ -320,8 +330,7 @@ def main():
     if rank == 0:
         sparsity = 1.0 - area_tot / (L * hq_loc * S * (S + 1) / 2)
         line = {
-            "metric": "pre-fill attention latency (ms), LLaMA-3-8B-1M attention, 32 layers mixed per-head "
-                      "patterns @128K" if args.config == "c2" else f"pre-fill attention latency (ms), {cfg['workload']}",
+            "metric": metric_name(args, cfg),
             "value": round(ms_per_step, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",

@@ -176,6 +176,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--gather", action="store_true",
+                    help="all-gather every layer's per-rank outputs into the full [Hq, S, d] on every rank "
+                         "(the optional collective of SURVEY 8e), inside the timed step")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.layers:
@@ -233,6 +236,9 @@ def main():
     lib = _lib.load()
 
     attn_events = []
+    from paper_2407_02490_b200.sharding import gather_heads
+
+    shards = [shard_heads(HQ, HKV, world, r) for r in range(world)]
 
     def step(record=False):
         for layer in range(L):
@@ -245,6 +251,8 @@ def main():
             if record:
                 e1.record(stream)
                 attn_events.append((e0, e1))
+            if args.gather and world > 1:
+                gather_heads(out, shards)
 
     # ---- warm-up + layout statistics (deterministic inputs -> fixed layouts) ----
     step()
@@ -342,7 +350,7 @@ def main():
                        "parallelism": f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
                                       f"divides {HKV}), no data-path collective",
                        "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
-                       "union_steps": union_tot},
+                       "union_steps": union_tot, "output_all_gather": bool(args.gather and world > 1)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -85,3 +85,21 @@ def test_c5_ashape_512k(P):
     out = kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), b, lay.tiles, lay.tile_offsets, lay.cols,
                                              lay.col_offsets)
     _check_rows(out, q, k, v, lay, s_len, b, _sampled_rows((s_len + b - 1) // b, 4))
+
+
+def test_c4_bs_256k(P):
+    from benchmarks.workloads import g_iid_qkv
+
+    from paper_2407_02490_b200 import kernels
+
+    s_len, d, b = 1 << 18, 128, 64
+    q, k, v = g_iid_qkv(1, 1, s_len, d, seed=9, device="cuda")
+    cfg = P.BlockSparse(100)
+    lay = P.build_layer_layout(q, k, [cfg], b)
+    rows = port.estimate_block_sparse(q[0].float().cpu().numpy(), k[0].float().cpu().numpy(), 100, b)
+    wt, wto = port.flatten(port.block_rows_to_tiles(rows, b))
+    np.testing.assert_array_equal(lay.tile_offsets.cpu().numpy(), wto)
+    np.testing.assert_array_equal(lay.tiles.cpu().numpy().astype(np.int64), wt)
+    out = kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), b, lay.tiles, lay.tile_offsets, lay.cols,
+                                             lay.col_offsets)
+    _check_rows(out, q, k, v, lay, s_len, b, _sampled_rows((s_len + b - 1) // b, 6))

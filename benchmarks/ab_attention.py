@@ -1,0 +1,38 @@
+"""A/B timing of two libspf builds on the same inputs, interleaved (attention only).
+
+    python benchmarks/ab_attention.py A/libspf.so B/libspf.so     # AB_CFG=vs|bs|as AB_SEQ=131072 AB_REPS=12
+
+Both libraries are loaded side by side with ctypes and launched alternately on one
+C2-shaped layer (32 q-heads, 8 kv, d=128, G-local), so clock and power drift hit
+both builds alike; prints the median times and their ratio.
+"""
+import ctypes, os, statistics, sys
+sys.path.insert(0, os.getcwd())
+import torch
+import paper_2407_02490_b200 as P
+from benchmarks.workloads import g_local_qkv
+libs = [ctypes.CDLL(os.path.abspath(p)) for p in sys.argv[1:3]]
+seq = int(os.environ.get("AB_SEQ", "131072"))
+q, k, v = g_local_qkv(32, 8, seq, 128, seed=0, device="cuda")
+cfg = os.environ.get("AB_CFG", "vs")
+cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * 32, "bs": [P.BlockSparse(100)] * 32, "as": [P.AShape(128, 4096)] * 32}[cfg]
+lay = P.build_layer_layout(q, k, cfgs, 64)
+out = torch.empty_like(q)
+vp = ctypes.c_void_p
+def run(lib):
+    lib.spf_sparse_flash_rows.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    rc = lib.spf_sparse_flash_rows(0, vp(q.data_ptr()), vp(k.data_ptr()), vp(v.data_ptr()), 32, 8, seq, 128,
+                                   ctypes.c_float(128 ** -0.5), 64, vp(lay.tiles.data_ptr()), vp(lay.tile_offsets.data_ptr()),
+                                   vp(lay.cols.data_ptr() if lay.cols.numel() else 0), vp(lay.col_offsets.data_ptr()),
+                                   vp(out.data_ptr()), None, 0, vp(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+ts = [[], []]
+for r in range(int(os.environ.get("AB_REPS", "12"))):
+    for i, lib in enumerate(libs):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); run(lib); e1.record(); torch.cuda.synchronize()
+        if r >= 2:
+            ts[i].append(e0.elapsed_time(e1))
+print(cfg, "A %.3f ms  B %.3f ms  (B/A %.3f)" % (statistics.median(ts[0]), statistics.median(ts[1]),
+                                             statistics.median(ts[1]) / statistics.median(ts[0])))

@@ -15,7 +15,8 @@ libs = [ctypes.CDLL(os.path.abspath(p)) for p in sys.argv[1:3]]
 seq = int(os.environ.get("AB_SEQ", "131072"))
 q, k, v = g_local_qkv(32, 8, seq, 128, seed=0, device="cuda")
 cfg = os.environ.get("AB_CFG", "vs")
-cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * 32, "bs": [P.BlockSparse(100)] * 32, "as": [P.AShape(128, 4096)] * 32}[cfg]
+cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * 32, "bs": [P.BlockSparse(100)] * 32, "as": [P.AShape(128, 4096)] * 32,
+        "tiny": [P.AShape(1, 64)] * 32, "small": [P.AShape(64, 640)] * 32}[cfg]
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p

@@ -106,7 +106,6 @@ struct Ctrl {
   // of another, and a single barrier would let its step-(t+1) arrivals complete
   // step t's phase before the slow warp's P(t) is in TMEM
   uint64_t p_full[2];
-  uint64_t pv_done;
   uint64_t o_ready;  // all PVs retired (committed once after the last one)
   uint32_t tmem_base;
   uint32_t pad;
@@ -229,7 +228,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     }
     mbar_init(&ctrl->p_full[0], 128 * kSoftHalves<kSplit>);
     mbar_init(&ctrl->p_full[1], 128 * kSoftHalves<kSplit>);
-    mbar_init(&ctrl->pv_done, 1);
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
   }
@@ -546,7 +544,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
             mma_bf16_ts_w2(tO, tP + 32 + k * 8, b_hi, dhi, idesc_pv, 1u);
           }
         }
-        mma_commit_w(&ctrl->pv_done);
         mma_commit_w(&ctrl->v_empty[sv]);
         if (kPvLag<kSplit> == 2) mma_commit_w(p_free(u & 1));
         if (!kSepP<kSplit>) mma_commit_w(&ctrl->s_free[u & 1]);
@@ -777,16 +774,17 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       const float sum = sa + sb2;
       l_run = l_run * alpha + sum;
 
-      // O rescale needs PV(t-1) retired.  S(t) being ready implies PV(t-2) retired (QK(t)
-      // is issued after PV(t-2) and the commit behind s_full tracks every earlier MMA of
-      // the issuing thread), so pv_done has completed t-1 or t phases: the parity wait for
-      // phase t-1 cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
+      // O rescale needs PV(t-1) retired: the V slot it read is released by a commit behind
+      // it (v_empty, phase (t-1)/kV).  S(t) being ready implies PV(t-2) retired (QK(t) is
+      // issued after PV(t-2) and the commit behind s_full tracks every earlier MMA of the
+      // issuing thread), so that slot's previous phase (PV(t-1-kV)) is complete and the
+      // parity wait cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
       // tcgen05.ld/st are warp-collective: decide per warp.
       if (t > 0 && __any_sync(0xffffffffu, rescale)) {
         if (kPvLag<kSplit> == 2)
           mbar_wait(p_free((t - 1) & 1), ((t - 1) >> 1) & 1);  // PV(t-1); PV(t-3) is retired: no aliasing
         else
-          mbar_wait(&ctrl->pv_done, (t - 1) & 1);
+          mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < kOCols; c += 32) {

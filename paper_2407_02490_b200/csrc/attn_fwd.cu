@@ -150,7 +150,8 @@ __device__ __forceinline__ void trace1(int role, int step, int ev) {
   unsigned long long* tr = g_trace1;
   if (tr == nullptr || (int)blockIdx.x >= g_trace1_ctas || step >= kTraceSteps1) return;
   unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (SPF_TRACE == 3) t = (unsigned long long)clock64();  // cycles (same SM throughout)
+  else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   tr[(((int64_t)blockIdx.x * 3 + role) * kTraceSteps1 + step) * 4 + ev] = t;
 }
 
@@ -616,9 +617,9 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     for (;; ++t) {
       const int sd = t % R::kD;
       const bool tr0 = warp == 2 && lane == 0;
-      if (tr0) trace1(1, t, 0);
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 0);
       mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
-      if (tr0) trace1(1, t, 1);
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 1);
       const StepDesc& d = ctrl->desc[sd];
       const int kind = d.kind;
       if (kind == kEnd) break;
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
       }
       tc_fence_after();
-      if (tr0) trace1(1, t, 2);
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 2);
       // lag 2: P buffer t&1 was last read by PV(t-2); S(t) ready only implies PV(t-3) retired
       auto wait_p_buffer = [&]() {
         if (kPvLag<kSplit> == 2 && t >= 2) {
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
       }
       tmem_wait_ld();
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, 0);
       if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
         tc_fence_before();
         __syncwarp();
@@ -729,6 +731,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         }
       }
       const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, __float_as_int(mx) == 0x7fc00001 ? 0 : 1);  // after the max
       float alpha = 1.f;
       bool rescale = false;
       if (hi > lo) {
@@ -769,6 +772,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           pl[j >> 1] = pack_bf16x2(p0 - hf.x, p1 - hf.y);
         }
       }
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, 2);  // after the exponentials
       float sa, sb2;
       unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
       const float sum = sa + sb2;

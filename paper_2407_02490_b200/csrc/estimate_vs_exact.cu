@@ -23,6 +23,7 @@
 // pass) lets an item be skipped when every score in it is below the row max
 // by more than 152 in log2 units: such p are < 2^-150 and round to exactly 0
 // in fp32 (l_i >= 1), i.e. the skip is exact, not an approximation.
+#include <algorithm>
 #include <cuda_bf16.h>
 
 #include "spf.h"
@@ -53,7 +54,11 @@ struct ExArgs {
   double* sscore;          // [n_heads][S]
   int32_t* list;           // fallback: significant items (h * n_kblk + kb) of the flagged heads
   int32_t* list_count;     // number of entries in list (device)
+  double* cache;           // fallback with L = KB = 64: pass A's scaled scores of list items [w][64][64]
+  int cache_items;         // items the cache holds (list positions >= this are recomputed)
 };
+
+constexpr int kCacheItems = 4096;  // 128 MB: the significant items of every flagged head at C2
 
 template <typename T>
 __device__ __forceinline__ double ld_f64(const T* p) {
@@ -238,7 +243,23 @@ __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restri
         for (int sb = 0; sb < KB / kKeyT; ++sb) {
           const int kk0 = k0 + sb * kKeyT;
           double acc[4][4];
-          score_tile(sm, qh, kh, r0, nrv, kk0, S, d, acc);
+          // pass B reuses pass A's fp64 scores of a listed item (bit-identical, no recompute)
+          const bool cached = listed && a.cache != nullptr && w < a.cache_items;
+          double* cw = cached ? a.cache + (size_t)w * (64 * 64) : nullptr;
+          if (kPass == 2 && cached) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[x][y] = cw[(4 * tr + x) * 64 + tk + 16 * y];
+          } else {
+            score_tile(sm, qh, kh, r0, nrv, kk0, S, d, acc);
+            if (kPass == 1 && cached) {
+#pragma unroll
+              for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) cw[(4 * tr + x) * 64 + tk + 16 * y] = acc[x][y];
+            }
+          }
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
             const int i = r0 + 4 * tr + x;
@@ -368,11 +389,19 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+static int cache_items_for(int n_heads, int seq_len, int last_q) {
+  const int KB = kb_for(last_q);
+  if (last_q != 64 || KB != 64) return 0;
+  const int64_t n = (int64_t)n_heads * ((seq_len + KB - 1) / KB);
+  return (int)std::min<int64_t>(n, kCacheItems);
+}
+
 size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q) {
   const int KB = kb_for(last_q);
   const size_t n_kblk = (seq_len + KB - 1) / KB;
   return al256((size_t)n_heads * last_q * n_kblk * 16) + al256((size_t)n_heads * last_q * 16) +
-         2 * al256((size_t)n_heads * seq_len * 8) + al256((size_t)n_heads * n_kblk * 4) + al256(4);
+         2 * al256((size_t)n_heads * seq_len * 8) + al256((size_t)n_heads * n_kblk * 4) + al256(4) +
+         al256((size_t)cache_items_for(n_heads, seq_len, last_q) * 64 * 64 * 8);
 }
 
 int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
@@ -405,6 +434,8 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
   a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   int32_t* list = reinterpret_cast<int32_t*>(take((size_t)n_heads * a.n_kblk * 4));
   int32_t* list_count = reinterpret_cast<int32_t*>(take(4));
+  const int cache_items = cache_items_for(n_heads, S, L);
+  double* cache = reinterpret_cast<double*>(take((size_t)cache_items * 64 * 64 * 8));
   const size_t smem = sizeof(ExSmem) + (size_t)(2 * a.KB + L - 1) * 8;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)a.n_kblk * n_heads, 148 * 4));
   int rc;
@@ -420,6 +451,8 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
       if ((rc = check_cuda(cudaMemsetAsync(list_count, 0, 4, st), "list count"))) return rc;
       a.list = list;
       a.list_count = list_count;
+      a.cache = cache_items > 0 ? cache : nullptr;
+      a.cache_items = cache_items;
       const int64_t warps = (int64_t)n_heads * a.n_kblk;
       note_launches(1);
       vs_exact_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);

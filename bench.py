@@ -239,6 +239,9 @@ def main():
     from paper_2407_02490_b200.sharding import gather_heads
 
     shards = [shard_heads(HQ, HKV, world, r) for r in range(world)]
+    from paper_2407_02490_b200.prefill import _pair_heads
+
+    pair_masks = [_pair_heads(cfgs[layer], dev) for layer in range(L)]  # Block-Sparse heads: paired-box kernel
 
     def step(record=False):
         for layer in range(L):
@@ -247,7 +250,7 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             kernels.sparse_flash_attention_gpu(Q[layer], K[layer], V[layer], scale, B, lay.tiles, lay.tile_offsets,
-                                               lay.cols, lay.col_offsets, out=out)
+                                               lay.cols, lay.col_offsets, out=out, pair_heads=pair_masks[layer])
             if record:
                 e1.record(stream)
                 attn_events.append((e0, e1))

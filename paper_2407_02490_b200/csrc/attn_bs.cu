@@ -1,0 +1,387 @@
+// attn_bs.cu -- paired-box sparse attention for heads whose two 64-row blocks per
+// 128-row CTA rarely share a tile (Block-Sparse heads: every block row picks its own
+// k_b key blocks), bf16 I/O.
+//
+// Same contract as attn_fwd.cu (_core.pyx:72-192: per 64-row block its tiles, per-cell
+// causal mask, one streaming-softmax state per row, zero rows without coverage); the
+// heads routed here have no residual columns (BS layouts never do).
+//
+// The union kernel (attn_fwd.cu) gives both row blocks of a CTA every tile of either,
+// so a BS CTA runs ~2 k_b steps of an M128 x N64 QK with half the rows masked.  Here a
+// step pairs the i-th tile of row block r0 with the i-th tile of row block r1 (both
+// walked from the diagonal down): one M128 x N128 x K=d QK (full tensor rate, where the
+// N64 one is shared-memory bound; profiles/r01/mma_pair_microbench.txt) whose rows
+// 0..63 keep the first 64 columns and rows 64..127 the last 64, and one M128 x N=d x
+// K128 PV with the off-block half of P zero.  Each thread still exponentiates 64 keys
+// per step, and there are max(n0, n1) steps instead of |tiles(r0) U tiles(r1)|.
+//
+// TMEM (256 columns, two CTAs per SM): S [0,128) fp32, P written back over its first
+// 64 columns as bf16 pairs, O [128,256).  With P over S, QK(t+1) is issued after PV(t)
+// (in-order pipe), so S(t) ready also implies PV(t-1) retired.  Shared memory: Q 32 KB,
+// one K and one V stage of two 64-key boxes (the chain leaves a whole softmax step for
+// the next loads).  An absent box (the shorter list ran out) is a TMA load past the
+// end of the sequence: zeros, masked out.
+#include "spf_internal.h"
+#include "spf_ptx.cuh"
+
+#include <math.h>
+
+namespace spf {
+
+namespace {
+
+constexpr int kRows = 128;
+constexpr int kBox = 64;
+constexpr int kKeys = 128;  // two boxes per step
+constexpr int kThreads = 192;
+
+struct PairDesc {
+  int box[2];    // first key of each box (-1: absent)
+  int width[2];  // keys of the box inside the sequence
+  int end;       // 1: no more steps
+};
+
+struct PCtrl {
+  uint64_t q_full;
+  uint64_t k_full, k_empty, v_full, v_empty;
+  uint64_t d_full[2], d_empty[2];
+  uint64_t s_full, p_full, o_ready;
+  uint32_t tmem_base, pad;
+  PairDesc desc[2];
+};
+
+template <int kD>
+struct PLayout {
+  static constexpr int kAtoms = kD / 64;
+  static constexpr int kQBytes = kRows * kD * 2;
+  static constexpr int kAtomStage = kKeys * 128;  // one 64-wide d atom of 128 keys (SW128 rows)
+  static constexpr int kStage = kAtoms * kAtomStage;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kQBytes;
+  static constexpr int kOffV = kOffK + kStage;
+  static constexpr int kOffCtrl = kOffV + kStage;
+  static constexpr int kSmem = kOffCtrl + (int)sizeof(PCtrl);
+  static constexpr uint32_t kTxBox = kBox * kD * 2;
+};
+
+__device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+
+template <int kD>
+__global__ void __launch_bounds__(kThreads, 2)
+    sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                            const __grid_constant__ CUtensorMap tm_v, const AttnArgs p, int n_ctile,
+                            float scale_log2) {
+  using L = PLayout<kD>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  PCtrl* ctrl = reinterpret_cast<PCtrl*>(smem + L::kOffCtrl);
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // work item: heavy (late) row tiles first, heads fastest; only the paired heads
+  const int item = blockIdx.x;
+  const int ct = n_ctile - 1 - item / p.Hq;
+  const int h = item % p.Hq;
+  if (p.pair_heads == nullptr || p.pair_heads[h] == 0) return;  // the union kernel's head
+  const int kvh = h / (p.Hq / p.Hkv);
+  const int S = p.S;
+  const int n_rows = (S + kBox - 1) / kBox;
+  const int R0 = ct * kRows;
+  const int r0 = R0 / kBox;
+  const bool has_r1 = r0 + 1 < n_rows;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&ctrl->q_full, 1);
+    mbar_init(&ctrl->k_full, 1);
+    mbar_init(&ctrl->k_empty, 1);
+    mbar_init(&ctrl->v_full, 1);
+    mbar_init(&ctrl->v_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&ctrl->d_full[s], 1);
+      mbar_init(&ctrl->d_empty[s], 4);
+    }
+    mbar_init(&ctrl->s_full, 1);
+    mbar_init(&ctrl->p_full, 128);
+    mbar_init(&ctrl->o_ready, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&ctrl->tmem_base, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctrl->tmem_base;
+
+  if (warp == 0) {
+    // =============================== loader warp ===============================
+    const int64_t row_a = (int64_t)h * n_rows + r0;
+    const int64_t a0 = p.tile_offsets[row_a], n0 = p.tile_offsets[row_a + 1] - a0;
+    const int64_t a1 = has_r1 ? p.tile_offsets[row_a + 1] : 0;
+    const int64_t n1 = has_r1 ? p.tile_offsets[row_a + 2] - a1 : 0;
+    const int64_t steps = n0 > n1 ? n0 : n1;
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_arrive_expect_tx(&ctrl->q_full, L::kQBytes);
+#pragma unroll
+      for (int a = 0; a < L::kAtoms; ++a)
+        tma_load_3d(smem + L::kOffQ + a * (kRows * 128), &tm_q, &ctrl->q_full, a * 64, R0, h);
+      for (int64_t i = 0; i <= steps; ++i) {
+        const int sd = (int)(i & 1);
+        mbar_wait(&ctrl->d_empty[sd], (int)((i >> 1) & 1) ^ 1);
+        PairDesc& d = ctrl->desc[sd];
+        if (i == steps) {
+          d.end = 1;
+          mbar_arrive(&ctrl->d_full[sd]);
+          break;
+        }
+        int box[2];
+        box[0] = i < n0 ? p.tile_starts[a0 + n0 - 1 - i] : -1;  // descending: the diagonal block first
+        box[1] = i < n1 ? p.tile_starts[a1 + n1 - 1 - i] : -1;
+        // K(i): free once QK(i-1) retired
+        mbar_wait(&ctrl->k_empty, (int)(i & 1) ^ 1);
+        mbar_arrive_expect_tx(&ctrl->k_full, 2 * L::kTxBox);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int row = box[b] >= 0 ? box[b] : S;  // absent: past the end -> zero fill
+#pragma unroll
+          for (int a = 0; a < L::kAtoms; ++a)
+            tma_load_3d(smem + L::kOffK + a * L::kAtomStage + b * (kBox * 128), &tm_k, &ctrl->k_full, a * 64, row,
+                        kvh);
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          d.box[b] = box[b];
+          d.width[b] = box[b] >= 0 ? min(kBox, S - box[b]) : 0;
+        }
+        d.end = 0;
+        mbar_arrive(&ctrl->d_full[sd]);
+        // V(i): free once PV(i-1) retired
+        mbar_wait(&ctrl->v_empty, (int)(i & 1) ^ 1);
+        mbar_arrive_expect_tx(&ctrl->v_full, 2 * L::kTxBox);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int row = box[b] >= 0 ? box[b] : S;
+#pragma unroll
+          for (int a = 0; a < L::kAtoms; ++a)
+            tma_load_3d(smem + L::kOffV + a * L::kAtomStage + b * (kBox * 128), &tm_v, &ctrl->v_full, a * 64, row,
+                        kvh);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // =============================== MMA issuer ================================
+    constexpr uint32_t idesc_qk = umma_idesc_bf16(128, kKeys, 0, 0);
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(128, kD, 0, 1);
+    const uint32_t tO = tmem + 128;
+    const uint32_t qlo0 = sw128_lo(sbase + L::kOffQ, 0);
+    const uint32_t klo0 = sw128_lo(sbase + L::kOffK, 0);
+    const uint32_t vlo0 = sw128_lo(sbase + L::kOffV, L::kAtomStage);  // LBO: next 64-wide d atom
+    constexpr uint32_t dhi = sw128_hi(1024);
+    mbar_wait(&ctrl->q_full, 0);
+    tc_fence_after();
+    int t = 0;
+    for (;; ++t) {
+      const int sd = t & 1;
+      mbar_wait(&ctrl->d_full[sd], (t >> 1) & 1);
+      if (*reinterpret_cast<volatile int*>(&ctrl->desc[sd].end)) break;
+      mbar_wait(&ctrl->k_full, t & 1);
+      tc_fence_after();
+      // S = Q K^T over 128 keys (the previous PV, issued earlier, has read P out of S)
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint32_t aoff = ((k >> 2) * (kRows * 128) + (k & 3) * 32) >> 4;
+        const uint32_t boff = ((k >> 2) * L::kAtomStage + (k & 3) * 32) >> 4;
+        mma_bf16_ss_w2(tmem, qlo0 + aoff, dhi, klo0 + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
+      }
+      mma_commit_w(&ctrl->s_full);
+      mma_commit_w(&ctrl->k_empty);
+      // O += P V over the step's 128 keys (P: bf16 pairs in S's columns 0..63)
+      mbar_wait(&ctrl->p_full, t & 1);
+      mbar_wait(&ctrl->v_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < kKeys / 16; ++k)
+        mma_bf16_ts_w2(tO, tmem + k * 8, vlo0 + ((k * 2048) >> 4), dhi, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
+      mma_commit_w(&ctrl->v_empty);
+    }
+    mma_commit_w(&ctrl->o_ready);
+    __syncwarp();
+  } else {
+    // =============================== softmax warps =============================
+    // rows 0..63 (lane quarters 0, 1) = row block r0 -> S columns 0..63 (box 0);
+    // rows 64..127 (quarters 2, 3) = row block r1 -> S columns 64..127 (box 1)
+    const int quarter = warp & 3;
+    const int half = quarter >> 1;
+    const int row = quarter * 32 + lane;
+    const int q = R0 + row;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    int t = 0;
+    for (;; ++t) {
+      const int sd = t & 1;
+      mbar_wait(&ctrl->d_full[sd], (t >> 1) & 1);
+      const PairDesc& d = ctrl->desc[sd];
+      if (d.end) break;
+      const int box = d.box[half];
+      int hi = 0;
+      if (box >= 0 && q < S) hi = min(d.width[half], q - box + 1);  // causal inside the block
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
+      const bool warp_skip = !__any_sync(0xffffffffu, hi > 0);
+      mbar_wait(&ctrl->s_full, t & 1);  // also orders this step's P write after QK(t)
+      tc_fence_after();
+      uint32_t ph[32];
+      float alpha = 1.f;
+      bool rescale = false;
+      if (!warp_skip) {
+        uint32_t x[kBox];
+        tmem_ld32x32b_x64(tmem + lane_off + half * kBox, x);
+        tmem_wait_ld();
+        if (hi < kBox) {
+#pragma unroll
+          for (int j = 0; j < kBox; ++j) x[j] = j < hi ? x[j] : 0xff800000u;
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kBox; j += 8) {
+          mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
+          mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
+          mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
+          mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
+        }
+        const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+        if (hi > 0) {
+          const float m_tile = mx * scale_log2;
+          if (m_run == -INFINITY) {
+            m_run = m_tile;
+          } else if (m_tile > m_run + 8.f) {
+            alpha = exp2f(m_run - m_tile);
+            m_run = m_tile;
+            rescale = true;
+          }
+        }
+        const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+        const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
+        const uint64_t m2 = pack_f32x2(neg_m, neg_m);
+        uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+        for (int j = 0; j < kBox; j += 2) {
+          const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
+          float y0, y1;
+          unpack_f32x2(yv, y0, y1);
+          const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+          const uint64_t pp = pack_f32x2(p0, p1);
+          switch ((j >> 1) & 3) {
+            case 0: s0 = fadd2(s0, pp); break;
+            case 1: s1 = fadd2(s1, pp); break;
+            case 2: s2 = fadd2(s2, pp); break;
+            default: s3 = fadd2(s3, pp); break;
+          }
+          ph[j >> 1] = pack_bf16x2(p0, p1);
+        }
+        float sa, sb;
+        unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb);
+        l_run = l_run * alpha + (sa + sb);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ph[j] = 0u;
+      }
+      // O rescale: S(t) ready implies PV(t-1) retired (issued before QK(t), in-order pipe)
+      if (t > 0 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t o[32];
+          tmem_ld32x32b_x32((tmem + lane_off + 128) + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
+          tmem_st32x32b_x32((tmem + lane_off + 128) + c, o);
+        }
+      }
+      // P row: this block's 64 keys, zeros for the other block's 64 (bf16 pairs, K-major)
+      uint32_t z[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = 0u;
+      tmem_st32x32b_x32(tmem + lane_off + half * 32, ph);
+      tmem_st32x32b_x32(tmem + lane_off + (half ^ 1) * 32, z);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&ctrl->p_full);
+    }
+    // ---- epilogue: O / l -> global (bf16) ----
+    mbar_wait(&ctrl->o_ready, 0);
+    tc_fence_after();
+    const float inv = (t > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+    const int dout = p.d_out;
+    const int64_t obase = ((int64_t)h * S + min(q, S - 1)) * dout;
+    if (p.lse != nullptr && q < S)
+      p.lse[(int64_t)h * S + q] = (t > 0 && l_run > 0.f) ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kD; c += 32) {
+      uint32_t o[32];
+      __syncwarp();
+      tmem_ld32x32b_x32((tmem + lane_off + 128) + c, o);
+      tmem_wait_ld();
+      if (q >= S) continue;
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + obase;
+      if (dout == kD) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          int4 w;
+          w.x = (int)pack_bf16x2(u2f(o[j]) * inv, u2f(o[j + 1]) * inv);
+          w.y = (int)pack_bf16x2(u2f(o[j + 2]) * inv, u2f(o[j + 3]) * inv);
+          w.z = (int)pack_bf16x2(u2f(o[j + 4]) * inv, u2f(o[j + 5]) * inv);
+          w.w = (int)pack_bf16x2(u2f(o[j + 6]) * inv, u2f(o[j + 7]) * inv);
+          *reinterpret_cast<int4*>(out + c + j) = w;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (c + j < dout) out[c + j] = __float2bfloat16_rn(u2f(o[j]) * inv);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+template <int kD>
+int launch_pair_impl(const AttnArgs& a, cudaStream_t stream) {
+  using L = PLayout<kD>;
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = make_tmap_bf16_3d(&tq, a.q_hi, kD, a.S, a.Hq, kRows))) return rc;
+  if ((rc = make_tmap_bf16_3d(&tk, a.k_hi, kD, a.S, a.Hkv, kBox))) return rc;
+  if ((rc = make_tmap_bf16_3d(&tv, a.v_hi, kD, a.S, a.Hkv, kBox))) return rc;
+  auto kern = sparse_attn_pair_kernel<kD>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem);
+    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(pair attn smem)");
+    attr_done = true;
+  }
+  const int n_ctile = (a.S + kRows - 1) / kRows;
+  const long long grid = (long long)n_ctile * a.Hq;
+  if (grid == 0) return 0;
+  if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
+  note_launches(1);
+  kern<<<(unsigned)grid, kThreads, L::kSmem, stream>>>(tq, tk, tv, a, n_ctile, a.scale * 1.4426950408889634f);
+  return check_cuda(cudaGetLastError(), "sparse_attn_pair launch");
+}
+
+}  // namespace
+
+bool attn_pair_supported(const AttnArgs& a) {
+  return !a.split && !a.out_f32 && a.B == kBox && (a.kD == 128 || a.kD == 64) && a.work_order == nullptr;
+}
+
+int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream) {
+  if (a.kD == 128) return launch_pair_impl<128>(a, stream);
+  return launch_pair_impl<64>(a, stream);
+}
+
+}  // namespace spf

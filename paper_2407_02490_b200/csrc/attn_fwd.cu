@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   if (p.work_order != nullptr) item = p.work_order[item];
   const int ct = n_ctile - 1 - item / p.Hq;
   const int h = item % p.Hq;
+  if (p.pair_heads != nullptr && p.pair_heads[h]) return;  // run by the paired-box kernel (attn_bs.cu)
   const int kvh = h / (p.Hq / p.Hkv);
   const int S = p.S, B = p.B;
   const int n_rows = (S + B - 1) / B;
@@ -941,7 +942,8 @@ int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream) {
     const char* e = getenv("SPF_ATTN_KERNEL");
     return e ? atoi(e) : 1;
   }();
-  if (kernel_choice == 2 && a.lse == nullptr && attn2_supported(a)) return launch_sparse_attn2(a, stream);
+  if (kernel_choice == 2 && a.lse == nullptr && a.pair_heads == nullptr && attn2_supported(a))
+    return launch_sparse_attn2(a, stream);
   if (a.kD == 128) return a.split ? launch_impl<128, true>(a, stream) : launch_impl<128, false>(a, stream);
   if (a.kD == 64) return a.split ? launch_impl<64, true>(a, stream) : launch_impl<64, false>(a, stream);
   return set_error(2, "padded head_dim must be 64 or 128 (got %d)", a.kD);

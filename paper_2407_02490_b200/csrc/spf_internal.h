@@ -34,9 +34,13 @@ struct AttnArgs {
   const int32_t* work_order;  // optional: CTA -> work-item list (nullptr = all items, heavy rows first)
   int n_work;                 // number of entries in work_order
   float* lse;                 // optional [Hq][S]: natural-log sum of exp(scale * q.k) over the row's cells
+  const uint8_t* pair_heads;  // optional [Hq]: 1 = run with the paired-box kernel (attn_bs.cu)
 };
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
+// Paired-box kernel for heads whose row blocks rarely share tiles (attn_bs.cu).
+bool attn_pair_supported(const AttnArgs& a);
+int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream);
 // Two-tile (256-row) bf16 kernel, attn_fwd2.cu.
 bool attn2_supported(const AttnArgs& a);
 int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream);

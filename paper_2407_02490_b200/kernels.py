@@ -42,13 +42,17 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                tile_starts: torch.Tensor, tile_offsets: torch.Tensor, col_indices: torch.Tensor,
                                col_offsets: torch.Tensor, out: torch.Tensor | None = None,
                                stream: torch.cuda.Stream | None = None,
-                               lse: torch.Tensor | None = None) -> torch.Tensor:
+                               lse: torch.Tensor | None = None,
+                               pair_heads: torch.Tensor | None = None) -> torch.Tensor:
     """Batched sparse FlashAttention on device tensors.
 
     q [Hq, S, d], k/v [Hkv, S, d] (bf16 or fp32, contiguous, same dtype);
     CSR over (head, row): offsets int64 [Hq*n_rows+1], entries int32.
     Returns out [Hq, S, d] in the input dtype.  ``lse`` (optional fp32 [Hq, S])
     receives each row's natural-log sum of exp(scale * q.k) over its cells.
+    ``pair_heads`` (optional uint8 [Hq] on the device) marks heads without residual
+    columns whose row blocks rarely share tiles (Block-Sparse heads): they run the
+    paired-box kernel (include/spf.h, spf_sparse_flash_rows_ex).
     """
     dev = _dev.require_cuda(q.device)
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
@@ -73,10 +77,12 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     cs = col_indices if col_indices.numel() else None
     if lse is not None and (lse.dtype != torch.float32 or lse.numel() != hq * s_len or not lse.is_contiguous()):
         raise ValueError("lse must be a contiguous fp32 [Hq, S] tensor")
-    _lib.check(lib.spf_sparse_flash_rows_lse(
+    if pair_heads is not None and (pair_heads.dtype != torch.uint8 or pair_heads.numel() != hq):
+        raise ValueError("pair_heads must be a uint8 [Hq] tensor")
+    _lib.check(lib.spf_sparse_flash_rows_ex(
         dtype, _dev.ptr(q), _dev.ptr(k), _dev.ptr(v), hq, hkv, s_len, d, float(scale), int(block_size),
-        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(out), _dev.ptr(lse),
-        _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows_lse")
+        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(pair_heads),
+        _dev.ptr(out), _dev.ptr(lse), _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows_ex")
     return out
 
 

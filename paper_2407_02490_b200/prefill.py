@@ -123,6 +123,24 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
     return LayerLayout(s_len, block_size, hq, tiles[:nt], toff, cols[:nc], coff)
 
 
+_PAIR_CACHE: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+
+
+def _pair_heads(head_cfgs, device):
+    """uint8 [Hq] mask of the Block-Sparse heads (no residual columns, row blocks that
+    rarely share tiles): the attention runs them with the paired-box kernel."""
+    key = (str(device), tuple(isinstance(c, BlockSparse) for c in head_cfgs))
+    if not any(key[1]):
+        return None
+    m = _PAIR_CACHE.get(key)
+    if m is None:
+        m = torch.tensor(key[1], dtype=torch.uint8, device=device)
+        _PAIR_CACHE[key] = m
+        if len(_PAIR_CACHE) > 64:
+            _PAIR_CACHE.popitem(last=False)
+    return m
+
+
 def sparse_prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, head_cfgs, block_size: int = 64,
                              scale: float | None = None, out: torch.Tensor | None = None, stream=None,
                              return_layout: bool = False, groups=None):
@@ -131,5 +149,6 @@ def sparse_prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, 
     d = q.shape[-1]
     sc = 1.0 / math.sqrt(d) if scale is None else float(scale)
     out = kernels.sparse_flash_attention_gpu(q, k, v, sc, block_size, layout.tiles, layout.tile_offsets,
-                                             layout.cols, layout.col_offsets, out=out, stream=stream)
+                                             layout.cols, layout.col_offsets, out=out, stream=stream,
+                                             pair_heads=_pair_heads(head_cfgs, q.device))
     return (out, layout) if return_layout else out

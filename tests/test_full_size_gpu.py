@@ -100,6 +100,7 @@ def test_c4_bs_256k(P):
     wt, wto = port.flatten(port.block_rows_to_tiles(rows, b))
     np.testing.assert_array_equal(lay.tile_offsets.cpu().numpy(), wto)
     np.testing.assert_array_equal(lay.tiles.cpu().numpy().astype(np.int64), wt)
-    out = kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), b, lay.tiles, lay.tile_offsets, lay.cols,
-                                             lay.col_offsets)
-    _check_rows(out, q, k, v, lay, s_len, b, _sampled_rows((s_len + b - 1) // b, 6))
+    for pair in (None, torch.ones(1, dtype=torch.uint8, device="cuda")):  # union and paired-box kernels
+        out = kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), b, lay.tiles, lay.tile_offsets, lay.cols,
+                                                 lay.col_offsets, pair_heads=pair)
+        _check_rows(out, q, k, v, lay, s_len, b, _sampled_rows((s_len + b - 1) // b, 6))

@@ -60,15 +60,6 @@ struct StepDesc {
 // step and keeps P over S with two S buffers: S/P [0,64) and [64,128), O [128,256).
 template <bool kSplit>
 constexpr bool kSepP = !kSplit;
-// PV lag (separate-P layout): PV(t-kPvLag) is issued right after QK(t).  Lag 2 keeps the
-// QK the next softmax step waits for from queueing behind a PV (S(t) ready then implies
-// only PV(t-3) retired; the P buffers get explicit "free" barriers) but measured 3.7%
-// slower than lag 1 on C2 (interleaved A/B, scratch-built), so lag 1 is the default.
-#ifndef SPF_PV_LAG
-#define SPF_PV_LAG 1
-#endif
-template <bool kSplit>
-constexpr int kPvLag = kSplit ? 1 : SPF_PV_LAG;
 
 // softmax warps per TMEM lane quarter.  2 (each thread exponentiates half a row, both
 // halves read the whole row for the max) was measured 14% slower than 1 on C2: more
@@ -97,9 +88,9 @@ struct Ctrl {
   uint64_t v_empty[Rings<kSplit>::kV];
   uint64_t d_full[Rings<kSplit>::kD];
   uint64_t d_empty[Rings<kSplit>::kD];
-  // split layout: S/P buffers 0 and 1.  Separate-P layout: s_full[0] / s_free[0] = the single
-  // S buffer written / read; s_full[1] / s_free[1] = P buffer 0 / 1 free (PV retired), used
-  // when kPvLag == 2 (see p_free()).
+  // split layout: S/P buffers 0 and 1.  Separate-P layout: [0] = the single S buffer
+  // written / read ([1] unused; PV issued two steps behind QK measured 3.7 % slower,
+  // profiles/r01/attn_bottleneck_experiments.txt).
   uint64_t s_full[2];
   uint64_t s_free[2];
   // P(t) written, one barrier per S/P buffer: a softmax warp can run one step ahead
@@ -233,7 +224,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
   }
-  auto p_free = [&](int b) -> uint64_t* { return b == 0 ? &ctrl->s_full[1] : &ctrl->s_free[1]; };
   if (warp == 1) tmem_alloc(&ctrl->tmem_base, 256);
   tc_fence_before();
   __syncthreads();
@@ -547,7 +537,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           }
         }
         mma_commit_w(&ctrl->v_empty[sv]);
-        if (kPvLag<kSplit> == 2) mma_commit_w(p_free(u & 1));
         if (!kSepP<kSplit>) mma_commit_w(&ctrl->s_free[u & 1]);
       };
 
@@ -588,10 +577,10 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           if (g_trace1 != nullptr && (int)blockIdx.x < g_trace1_ctas && t < kTraceSteps1)
             g_trace1[(((int64_t)blockIdx.x * 3 + 2) * kTraceSteps1 + t) * 4 + 0] = (unsigned long long)dc;
         }
-        if (t >= kPvLag<kSplit>) issue_pv(t - kPvLag<kSplit>);
-        if (lane == 0 && t >= kPvLag<kSplit>) trace1(0, t - kPvLag<kSplit>, 3);
+        if (t > 0) issue_pv(t - 1);
+        if (lane == 0 && t > 0) trace1(0, t - 1, 3);
       }
-      for (int u = max(0, t - kPvLag<kSplit>); u < t; ++u) issue_pv(u);
+      if (t > 0) issue_pv(t - 1);
       mma_commit_w(&ctrl->o_ready);
     }
     __syncwarp();
@@ -633,12 +622,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       tc_fence_after();
       if (tr0 && SPF_TRACE != 3) trace1(1, t, 2);
       // lag 2: P buffer t&1 was last read by PV(t-2); S(t) ready only implies PV(t-3) retired
-      auto wait_p_buffer = [&]() {
-        if (kPvLag<kSplit> == 2 && t >= 2) {
-          mbar_wait(p_free(sb), ((t - 2) >> 1) & 1);
-          tc_fence_after();
-        }
-      };
       if (SPF_EXPT == 2 || SPF_EXPT == 6) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
@@ -688,7 +671,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         uint32_t z[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) z[j] = 0u;
-        wait_p_buffer();
         if (kSepP<kSplit>) {
           const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
           if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, z);
@@ -786,10 +768,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       // parity wait cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
       // tcgen05.ld/st are warp-collective: decide per warp.
       if (t > 0 && __any_sync(0xffffffffu, rescale)) {
-        if (kPvLag<kSplit> == 2)
-          mbar_wait(p_free((t - 1) & 1), ((t - 1) >> 1) & 1);  // PV(t-1); PV(t-3) is retired: no aliasing
-        else
-          mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
+        mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < kOCols; c += 32) {
@@ -802,7 +781,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         }
       }
       // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
-      wait_p_buffer();
       if (kSepP<kSplit>) {
         const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
         if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);

@@ -34,6 +34,7 @@ struct BlockTopK {
   static constexpr int kKeyBits = sizeof(Key) * 8;
   using Scan = cub::BlockScan<int, kThreads>;
 
+  static constexpr int kWarps = kThreads / 32;
   struct Storage {
     int hist[kBins];
     typename Scan::TempStorage scan;
@@ -41,6 +42,7 @@ struct BlockTopK {
     int krem;
     int force_pos;
     int force_sel;
+    int wcnt[2][kWarps];  // per-warp T-valued / selected counts (index-ordered passes)
   };
 
   // vals: n candidates (global or shared).  Writes k_eff = min(k, n) indices to out.
@@ -68,10 +70,14 @@ struct BlockTopK {
           hit = (key & pmask) == prefix;
           dig = (int)((key >> sh) & dmask);
         }
+        // lanes sharing the first active lane's digit add once; the rest add singly
         const unsigned act = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const unsigned peers = __match_any_sync(act, dig);
-          if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sm.hist[dig], __popc(peers));
+        if (act) {
+          const int lead = __ffs(act) - 1;
+          const int ldig = __shfl_sync(0xffffffffu, dig, lead);
+          const unsigned same = __ballot_sync(0xffffffffu, hit && dig == ldig);
+          if ((threadIdx.x & 31) == lead) atomicAdd(&sm.hist[ldig], __popc(same));
+          else if (hit && dig != ldig) atomicAdd(&sm.hist[dig], 1);
         }
       }
       __syncthreads();
@@ -105,70 +111,93 @@ struct BlockTopK {
       __syncthreads();
     }
     const Key thr = prefix;  // exact k-th largest key; krem T-valued elements are taken
-    // force-include bookkeeping: is force_idx selected?  (its equal-rank is
-    // irrelevant unless key == thr; we compute it in the ordered pass.)
-    const int chunk = (n + kThreads - 1) / kThreads;
-    const int b0 = min(n, tid * chunk), b1 = min(n, b0 + chunk);
-    int eq = 0;
-    for (int i = b0; i < b1; ++i) eq += (mono_key(vals[i]) == thr);
-    int eq_base;
-    Scan(sm.scan).ExclusiveSum(eq, eq_base);
-    __syncthreads();
-    // pass 1: is force_idx selected?
-    if (force_idx >= b0 && force_idx < b1) {
-      const Key kf = mono_key(vals[force_idx]);
-      int r = eq_base;
-      for (int i = b0; i < force_idx; ++i) r += (mono_key(vals[i]) == thr);
-      sm.force_sel = (kf > thr) || (kf == thr && r < krem);
+    // Index-ordered passes, warp-cooperative: warp w owns a contiguous range of 32-element
+    // groups, lanes read consecutive elements (coalesced, no bank conflicts) and the
+    // in-order ranks come from ballots; per-warp totals are prefixed over the warps.
+    const int lane = tid & 31, w = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int wchunk = (((n + kWarps - 1) / kWarps) + 31) & ~31;
+    const int w0 = min(n, w * wchunk), w1 = min(n, w0 + wchunk);
+    // pass A: T-valued count per warp
+    int eqc = 0;
+    for (int base = w0; base < w1; base += 32) {
+      const int i = base + lane;
+      eqc += __popc(__ballot_sync(0xffffffffu, i < w1 && mono_key(vals[i]) == thr));
     }
-    if (force_idx < 0 || force_idx >= n) {
-      if (tid == 0) sm.force_sel = 1;
+    if (lane == 0) sm.wcnt[0][w] = eqc;
+    if (tid == 0) sm.force_sel = (force_idx < 0 || force_idx >= n) ? 1 : 0;
+    __syncthreads();
+    int eq_base = 0;
+    for (int x = 0; x < w; ++x) eq_base += sm.wcnt[0][x];
+    // is force_idx selected?  (the warp owning it ranks it among the T-valued keys)
+    if (force_idx >= w0 && force_idx < w1) {
+      int r = eq_base;
+      for (int base = w0; base <= force_idx; base += 32) {
+        const int i = base + lane;
+        const unsigned em = __ballot_sync(0xffffffffu, i < w1 && mono_key(vals[i]) == thr);
+        if (force_idx < base + 32) {
+          const Key kf = mono_key(vals[force_idx]);
+          const int rf = r + __popc(em & ((1u << (force_idx - base)) - 1u));
+          if (lane == 0) sm.force_sel = (kf > thr) || (kf == thr && rf < krem);
+        }
+        r += __popc(em);
+      }
     }
     __syncthreads();
     const bool need_force = !sm.force_sel;
     const int quota = need_force ? krem - 1 : krem;  // the weakest (rank krem-1) makes room
-    // pass 2: count selected per chunk, excluding force_idx (placed separately)
-    int sel = 0;
+    auto selected = [&](int i, int base, int r, unsigned em, Key key) {
+      const bool is_eq = i < w1 && key == thr;
+      const bool s = i < w1 && ((key > thr) || (is_eq && r + __popc(em & lt) < quota));
+      return s && !(need_force && i == force_idx);
+    };
+    // pass B: selected count per warp (force_idx, when forced, is placed separately)
+    int selc = 0;
     {
       int r = eq_base;
-      for (int i = b0; i < b1; ++i) {
-        const Key key = mono_key(vals[i]);
-        const bool is_eq = key == thr;
-        const bool s = (key > thr) || (is_eq && r < quota);
-        r += is_eq;
-        sel += (s && !(need_force && i == force_idx)) ? 1 : 0;
+      for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        const Key key = i < w1 ? mono_key(vals[i]) : (Key)0;
+        const unsigned em = __ballot_sync(0xffffffffu, i < w1 && key == thr);
+        selc += __popc(__ballot_sync(0xffffffffu, selected(i, base, r, em, key)));
+        r += __popc(em);
       }
     }
-    int sel_base;
-    Scan(sm.scan).ExclusiveSum(sel, sel_base);
+    if (lane == 0) sm.wcnt[1][w] = selc;
     __syncthreads();
-    if (need_force && force_idx >= b0 && force_idx < b1) {
-      int before = sel_base;
-      int r = eq_base;
-      for (int i = b0; i < force_idx; ++i) {
-        const Key key = mono_key(vals[i]);
-        const bool is_eq = key == thr;
-        before += ((key > thr) || (is_eq && r < quota)) ? 1 : 0;
-        r += is_eq;
+    int sel_base = 0;
+    for (int x = 0; x < w; ++x) sel_base += sm.wcnt[1][x];
+    // forced index: its slot = selected elements before it in index order
+    if (need_force && force_idx >= w0 && force_idx < w1) {
+      int r = eq_base, before = sel_base;
+      for (int base = w0; base <= force_idx; base += 32) {
+        const int i = base + lane;
+        const Key key = i < w1 ? mono_key(vals[i]) : (Key)0;
+        const unsigned em = __ballot_sync(0xffffffffu, i < w1 && key == thr);
+        const unsigned sm_ = __ballot_sync(0xffffffffu, selected(i, base, r, em, key));
+        before += __popc(force_idx < base + 32 ? (sm_ & ((1u << (force_idx - base)) - 1u)) : sm_);
+        r += __popc(em);
       }
-      sm.force_pos = before;
+      if (lane == 0) sm.force_pos = before;
     }
     __syncthreads();
     const int fpos = need_force ? sm.force_pos : -1;
-    // pass 3: write in index order
+    // pass C: write in index order
     {
-      int r = eq_base;
-      int pos = sel_base;
-      for (int i = b0; i < b1; ++i) {
-        const Key key = mono_key(vals[i]);
-        const bool is_eq = key == thr;
-        const bool s = ((key > thr) || (is_eq && r < quota)) && !(need_force && i == force_idx);
-        r += is_eq;
+      int r = eq_base, pos = sel_base;
+      for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        const Key key = i < w1 ? mono_key(vals[i]) : (Key)0;
+        const unsigned em = __ballot_sync(0xffffffffu, i < w1 && key == thr);
+        const bool s = selected(i, base, r, em, key);
+        const unsigned smask = __ballot_sync(0xffffffffu, s);
         if (s) {
-          const int slot = pos + ((need_force && pos >= fpos) ? 1 : 0);
+          const int p0 = pos + __popc(smask & lt);
+          const int slot = p0 + ((need_force && p0 >= fpos) ? 1 : 0);
           out[descending ? (k - 1 - slot) : slot] = i * out_scale;
-          ++pos;
         }
+        pos += __popc(smask);
+        r += __popc(em);
       }
     }
     if (need_force && tid == 0) out[descending ? (k - 1 - fpos) : fpos] = force_idx * out_scale;

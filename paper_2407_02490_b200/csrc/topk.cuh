@@ -29,7 +29,9 @@ __device__ __forceinline__ uint32_t mono_key(float v) {
 template <int kThreads, typename T>
 struct BlockTopK {
   using Key = typename std::conditional<sizeof(T) == 8, uint64_t, uint32_t>::type;
-  static constexpr int kBits = 11;
+  // 8-bit digits: a 256-bin histogram is zeroed and scanned with one bin per thread (rows
+  // of a few thousand candidates pay more for 2048-bin rounds than for one extra round)
+  static constexpr int kBits = 8;
   static constexpr int kBins = 1 << kBits;
   static constexpr int kKeyBits = sizeof(Key) * 8;
   using Scan = cub::BlockScan<int, kThreads>;

@@ -41,11 +41,23 @@ struct PairDesc {
   int end;       // 1: no more steps
 };
 
+// !kDB (the default): two CTAs per SM, one S with P written over it -- a serial
+// softmax -> PV -> QK chain per CTA that the co-resident CTA interleaves with.
+// kDB (SPF_PAIR_DB=1): one CTA per SM owning all 512 TMEM columns -- S(t) in
+// [128 (t&1), +128), O [256,384), P(t) in [384 + 64 (t&1), +64) -- so QK(t+1) overlaps the
+// softmax of step t; identical results, but measured 10-14 % slower than two interleaved
+// CTAs (profiles/r01/attn_bottleneck_experiments.txt).
+#ifndef SPF_PAIR_DB
+#define SPF_PAIR_DB 0
+#endif
+constexpr bool kDB = SPF_PAIR_DB != 0;
+constexpr int kStages = kDB ? 2 : 1;
+
 struct PCtrl {
   uint64_t q_full;
-  uint64_t k_full, k_empty, v_full, v_empty;
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t d_full[2], d_empty[2];
-  uint64_t s_full, p_full, o_ready;
+  uint64_t s_full[2], s_free[2], p_full[2], o_ready;
   uint32_t tmem_base, pad;
   PairDesc desc[2];
 };
@@ -58,16 +70,21 @@ struct PLayout {
   static constexpr int kStage = kAtoms * kAtomStage;
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + kQBytes;
-  static constexpr int kOffV = kOffK + kStage;
-  static constexpr int kOffCtrl = kOffV + kStage;
+  static constexpr int kOffV = kOffK + kStages * kStage;
+  static constexpr int kOffCtrl = kOffV + kStages * kStage;
   static constexpr int kSmem = kOffCtrl + (int)sizeof(PCtrl);
   static constexpr uint32_t kTxBox = kBox * kD * 2;
+  static constexpr uint32_t kTmemCols = kDB ? 512 : 256;
+  static constexpr uint32_t kColO = kDB ? 256 : 128;
 };
+// TMEM column of S(t) / P(t)
+__device__ __forceinline__ uint32_t s_col(int t) { return kDB ? (uint32_t)(t & 1) * 128 : 0u; }
+__device__ __forceinline__ uint32_t p_col(int t) { return kDB ? 384u + (uint32_t)(t & 1) * 64 : 0u; }
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
 template <int kD>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                             const __grid_constant__ CUtensorMap tm_v, const AttnArgs p, int n_ctile,
                             float scale_log2) {
@@ -91,20 +108,21 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (threadIdx.x == 0) {
     mbar_init(&ctrl->q_full, 1);
-    mbar_init(&ctrl->k_full, 1);
-    mbar_init(&ctrl->k_empty, 1);
-    mbar_init(&ctrl->v_full, 1);
-    mbar_init(&ctrl->v_empty, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&ctrl->k_full[s], 1);
+      mbar_init(&ctrl->k_empty[s], 1);
+      mbar_init(&ctrl->v_full[s], 1);
+      mbar_init(&ctrl->v_empty[s], 1);
       mbar_init(&ctrl->d_full[s], 1);
       mbar_init(&ctrl->d_empty[s], 4);
+      mbar_init(&ctrl->s_full[s], 1);
+      mbar_init(&ctrl->s_free[s], 4);
+      mbar_init(&ctrl->p_full[s], 128);
     }
-    mbar_init(&ctrl->s_full, 1);
-    mbar_init(&ctrl->p_full, 128);
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&ctrl->tmem_base, 256);
+  if (warp == 1) tmem_alloc(&ctrl->tmem_base, L::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -137,16 +155,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         int box[2];
         box[0] = i < n0 ? p.tile_starts[a0 + n0 - 1 - i] : -1;  // descending: the diagonal block first
         box[1] = i < n1 ? p.tile_starts[a1 + n1 - 1 - i] : -1;
-        // K(i): free once QK(i-1) retired
-        mbar_wait(&ctrl->k_empty, (int)(i & 1) ^ 1);
-        mbar_arrive_expect_tx(&ctrl->k_full, 2 * L::kTxBox);
+        // K(i): its stage is free once QK(i - kStages) retired
+        const int st = (int)(i % kStages);
+        const int sph = (int)((i / kStages) & 1);
+        mbar_wait(&ctrl->k_empty[st], sph ^ 1);
+        mbar_arrive_expect_tx(&ctrl->k_full[st], 2 * L::kTxBox);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int row = box[b] >= 0 ? box[b] : S;  // absent: past the end -> zero fill
 #pragma unroll
           for (int a = 0; a < L::kAtoms; ++a)
-            tma_load_3d(smem + L::kOffK + a * L::kAtomStage + b * (kBox * 128), &tm_k, &ctrl->k_full, a * 64, row,
-                        kvh);
+            tma_load_3d(smem + L::kOffK + st * L::kStage + a * L::kAtomStage + b * (kBox * 128), &tm_k,
+                        &ctrl->k_full[st], a * 64, row, kvh);
         }
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
@@ -155,16 +175,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         d.end = 0;
         mbar_arrive(&ctrl->d_full[sd]);
-        // V(i): free once PV(i-1) retired
-        mbar_wait(&ctrl->v_empty, (int)(i & 1) ^ 1);
-        mbar_arrive_expect_tx(&ctrl->v_full, 2 * L::kTxBox);
+        // V(i): its stage is free once PV(i - kStages) retired
+        mbar_wait(&ctrl->v_empty[st], sph ^ 1);
+        mbar_arrive_expect_tx(&ctrl->v_full[st], 2 * L::kTxBox);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int row = box[b] >= 0 ? box[b] : S;
 #pragma unroll
           for (int a = 0; a < L::kAtoms; ++a)
-            tma_load_3d(smem + L::kOffV + a * L::kAtomStage + b * (kBox * 128), &tm_v, &ctrl->v_full, a * 64, row,
-                        kvh);
+            tma_load_3d(smem + L::kOffV + st * L::kStage + a * L::kAtomStage + b * (kBox * 128), &tm_v,
+                        &ctrl->v_full[st], a * 64, row, kvh);
         }
       }
     }
@@ -173,38 +193,50 @@ __global__ void __launch_bounds__(kThreads, 2)
     // =============================== MMA issuer ================================
     constexpr uint32_t idesc_qk = umma_idesc_bf16(128, kKeys, 0, 0);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, kD, 0, 1);
-    const uint32_t tO = tmem + 128;
+    const uint32_t tO = tmem + L::kColO;
     const uint32_t qlo0 = sw128_lo(sbase + L::kOffQ, 0);
     const uint32_t klo0 = sw128_lo(sbase + L::kOffK, 0);
     const uint32_t vlo0 = sw128_lo(sbase + L::kOffV, L::kAtomStage);  // LBO: next 64-wide d atom
     constexpr uint32_t dhi = sw128_hi(1024);
     mbar_wait(&ctrl->q_full, 0);
     tc_fence_after();
+    auto issue_pv = [&](int u) {  // O += P(u) V(u) over the step's 128 keys
+      const int st = u % kStages;
+      mbar_wait(&ctrl->p_full[u & 1], (u >> 1) & 1);
+      mbar_wait(&ctrl->v_full[st], (u / kStages) & 1);
+      tc_fence_after();
+      const uint32_t vd = vlo0 + ((uint32_t)(st * L::kStage) >> 4);
+#pragma unroll
+      for (int k = 0; k < kKeys / 16; ++k)
+        mma_bf16_ts_w2(tO, tmem + p_col(u) + k * 8, vd + ((k * 2048) >> 4), dhi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
+      mma_commit_w(&ctrl->v_empty[st]);
+    };
     int t = 0;
     for (;; ++t) {
       const int sd = t & 1;
       mbar_wait(&ctrl->d_full[sd], (t >> 1) & 1);
       if (*reinterpret_cast<volatile int*>(&ctrl->desc[sd].end)) break;
-      mbar_wait(&ctrl->k_full, t & 1);
+      const int st = t % kStages;
+      mbar_wait(&ctrl->k_full[st], (t / kStages) & 1);
+      if (kDB && t >= 2) mbar_wait(&ctrl->s_free[t & 1], ((t - 2) >> 1) & 1);  // softmax(t-2) read S
       tc_fence_after();
-      // S = Q K^T over 128 keys (the previous PV, issued earlier, has read P out of S)
+      // S(t) = Q K^T over 128 keys (single-buffered: the previous PV has read P out of S)
+      const uint32_t kd = klo0 + ((uint32_t)(st * L::kStage) >> 4);
 #pragma unroll
       for (int k = 0; k < kD / 16; ++k) {
         const uint32_t aoff = ((k >> 2) * (kRows * 128) + (k & 3) * 32) >> 4;
         const uint32_t boff = ((k >> 2) * L::kAtomStage + (k & 3) * 32) >> 4;
-        mma_bf16_ss_w2(tmem, qlo0 + aoff, dhi, klo0 + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
+        mma_bf16_ss_w2(tmem + s_col(t), qlo0 + aoff, dhi, kd + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
       }
-      mma_commit_w(&ctrl->s_full);
-      mma_commit_w(&ctrl->k_empty);
-      // O += P V over the step's 128 keys (P: bf16 pairs in S's columns 0..63)
-      mbar_wait(&ctrl->p_full, t & 1);
-      mbar_wait(&ctrl->v_full, t & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int k = 0; k < kKeys / 16; ++k)
-        mma_bf16_ts_w2(tO, tmem + k * 8, vlo0 + ((k * 2048) >> 4), dhi, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
-      mma_commit_w(&ctrl->v_empty);
+      mma_commit_w(&ctrl->s_full[t & 1]);
+      mma_commit_w(&ctrl->k_empty[st]);
+      if (kDB) {
+        if (t > 0) issue_pv(t - 1);  // PV(t-1) behind QK(t): the next S is never late for PV
+      } else {
+        issue_pv(t);
+      }
     }
+    if (kDB && t > 0) issue_pv(t - 1);
     mma_commit_w(&ctrl->o_ready);
     __syncwarp();
   } else {
@@ -229,14 +261,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
       const bool warp_skip = !__any_sync(0xffffffffu, hi > 0);
-      mbar_wait(&ctrl->s_full, t & 1);  // also orders this step's P write after QK(t)
+      mbar_wait(&ctrl->s_full[t & 1], (t >> 1) & 1);  // also orders P(t) after QK(t)
       tc_fence_after();
       uint32_t ph[32];
       float alpha = 1.f;
       bool rescale = false;
       if (!warp_skip) {
         uint32_t x[kBox];
-        tmem_ld32x32b_x64(tmem + lane_off + half * kBox, x);
+        tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + half * kBox, x);
         tmem_wait_ld();
         if (hi < kBox) {
 #pragma unroll
@@ -287,27 +319,39 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int j = 0; j < 32; ++j) ph[j] = 0u;
       }
-      // O rescale: S(t) ready implies PV(t-1) retired (issued before QK(t), in-order pipe)
+      if (kDB) {  // S(t) consumed (QK(t+2) may overwrite it)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->s_free[t & 1]);
+      }
+      // O rescale needs PV(t-1) retired: in the single-buffered chain S(t) ready implies it;
+      // double-buffered, S(t) implies PV(t-2), so wait for PV(t-1)'s V-stage release (the
+      // previous phase of that stage, PV(t-3), is retired: no aliasing)
       if (t > 0 && __any_sync(0xffffffffu, rescale)) {
+        if (kDB) {
+          mbar_wait(&ctrl->v_empty[(t - 1) % kStages], ((t - 1) / kStages) & 1);
+          tc_fence_after();
+        }
 #pragma unroll
         for (int c = 0; c < kD; c += 32) {
           uint32_t o[32];
-          tmem_ld32x32b_x32((tmem + lane_off + 128) + c, o);
+          tmem_ld32x32b_x32((tmem + lane_off + L::kColO) + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-          tmem_st32x32b_x32((tmem + lane_off + 128) + c, o);
+          tmem_st32x32b_x32((tmem + lane_off + L::kColO) + c, o);
         }
       }
       // P row: this block's 64 keys, zeros for the other block's 64 (bf16 pairs, K-major)
       uint32_t z[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) z[j] = 0u;
-      tmem_st32x32b_x32(tmem + lane_off + half * 32, ph);
-      tmem_st32x32b_x32(tmem + lane_off + (half ^ 1) * 32, z);
+      // P(t)'s buffer was last read by PV(t-2), retired before QK(t) completed
+      tmem_st32x32b_x32(tmem + lane_off + p_col(t) + half * 32, ph);
+      tmem_st32x32b_x32(tmem + lane_off + p_col(t) + (half ^ 1) * 32, z);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&ctrl->p_full);
+      mbar_arrive(&ctrl->p_full[t & 1]);
     }
     // ---- epilogue: O / l -> global (bf16) ----
     mbar_wait(&ctrl->o_ready, 0);
@@ -321,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int c = 0; c < kD; c += 32) {
       uint32_t o[32];
       __syncwarp();
-      tmem_ld32x32b_x32((tmem + lane_off + 128) + c, o);
+      tmem_ld32x32b_x32((tmem + lane_off + L::kColO) + c, o);
       tmem_wait_ld();
       if (q >= S) continue;
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + obase;
@@ -345,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, L::kTmemCols);
   }
 }
 

@@ -142,3 +142,43 @@ def test_multihead_bf16_gqa(K, s, hq, hkv, b):
         want = port.sparse_flash_rows(q[h], k[kvh], v[kvh], 1 / math.sqrt(d), b, ts, to[sl], cs, co[sl])
         worst = max(worst, max_abs(out[h], want))
     assert worst <= BF16_TOL, worst
+
+
+@pytest.mark.parametrize("s,kb,d", [(1000, 3, 128), (4097, 8, 128), (63, 2, 64), (3000, 1, 64)])
+def test_paired_box_kernel_matches_oracle(K, s, kb, d):
+    """The paired-box kernel (Block-Sparse heads, pair_heads) on block-sparse layouts with
+    an odd number of row blocks, rows shorter than k_b, k_b = 1 (diagonal only) and a
+    sub-block sequence: every row equals the oracle kernel; unflagged heads in the same
+    launch still run the union kernel."""
+    hq, hkv, b = 4, 2, 64
+    rng = np.random.Generator(np.random.PCG64(s + kb))
+    q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    v = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    n = (s + b - 1) // b
+    tiles_all = []
+    for h in range(hq):
+        for r in range(n):
+            m = min(kb, r + 1)
+            blocks = sorted(set([r] + rng.choice(r + 1, size=m, replace=False).tolist()))[-m:]
+            if r not in blocks:
+                blocks[-1] = r
+            tiles_all.append(sorted(x * b for x in blocks))
+    ts, to = port.flatten(tiles_all)
+    co = np.zeros(hq * n + 1, np.int64)
+    dev = torch.device("cuda")
+    pair = torch.tensor([1, 0, 1, 1], dtype=torch.uint8, device=dev)
+    args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+            torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+            torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+            torch.zeros(1, dtype=torch.int32, device=dev), torch.from_numpy(co).to(dev))
+    got = K.sparse_flash_attention_gpu(*args, pair_heads=pair).float().cpu().numpy()
+    union = K.sparse_flash_attention_gpu(*args).float().cpu().numpy()
+    for h in range(hq):
+        kvh = h // (hq // hkv)
+        t0, t1 = h * n, (h + 1) * n
+        tt, tto = port.flatten(tiles_all[t0:t1])
+        want = port.sparse_flash_rows(q[h], k[kvh], v[kvh], 1 / math.sqrt(d), b, tt, tto,
+                                      np.zeros(0, np.int64), np.zeros(n + 1, np.int64))
+        assert np.abs(got[h] - want).max() < BF16_TOL, (h, np.abs(got[h] - want).max())
+        assert np.abs(got[h] - union[h]).max() < BF16_TOL

@@ -86,6 +86,15 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
                              const uint8_t* pair_heads, void* out, float* lse_out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * argtopk (estimator.py:59-67): indices of the k largest values in descending-value
+ * order, ties toward the lower index (np.argsort(-x, kind="stable")[:k]; -0.0 == 0.0).
+ * values: device fp64 [n]; out: device int32 [min(k, n)]; k <= 16384.
+ * ------------------------------------------------------------------------- */
+size_t spf_argtopk_workspace_size(int64_t n);
+int spf_argtopk(const double* values, int64_t n, int k, int32_t* out, void* workspace, size_t workspace_bytes,
+                void* stream);
+
 /* Heads selection: the estimation and layout entry points below work on a
  * subset of q-heads given by `head_ids` (device int32 [n_heads]; NULL means
  * heads 0..n_heads-1) so a layer whose heads use different patterns fills

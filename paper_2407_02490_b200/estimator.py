@@ -68,15 +68,30 @@ class BlockIndices:
                 raise ValueError(f"row {r}: block index outside causal range")
 
 
+ARGTOPK_MAX_K = 16384
+
+
 def argtopk(values, k: int) -> np.ndarray:
     """estimator.py:59-67: indices of the k largest values in descending-value
-    order, ties toward the smaller index (device stable sort)."""
+    order, ties toward the smaller index -- spf_argtopk (radix select + bitonic
+    ordering of the k picks on the device)."""
     if k < 1:
         raise ValueError("k must be >= 1")
     dev = _dev.require_cuda()
-    vals = torch.as_tensor(np.asarray(values, dtype=np.float64), device=dev)
-    order = torch.sort(vals, descending=True, stable=True).indices
-    return order[: min(k, vals.numel())].cpu().numpy().astype(np.int64)
+    vals = torch.as_tensor(np.asarray(values, dtype=np.float64).reshape(-1), device=dev).contiguous()
+    n = int(vals.numel())
+    m = min(int(k), n)
+    if m == 0:
+        return np.zeros(0, dtype=np.int64)
+    if m > ARGTOPK_MAX_K:
+        raise ValueError(f"argtopk supports k <= {ARGTOPK_MAX_K} on the device (got {m})")
+    lib = _lib.load()
+    out = torch.empty(m, dtype=torch.int32, device=dev)
+    ws_bytes = lib.spf_argtopk_workspace_size(n)
+    ws = _dev.workspace(ws_bytes, dev)
+    _lib.check(lib.spf_argtopk(_dev.ptr(vals), n, m, _dev.ptr(out), _dev.ptr(ws), ws_bytes, _dev.stream_handle()),
+               "spf_argtopk")
+    return out.cpu().numpy().astype(np.int64)
 
 
 def _dtype_code(t: torch.Tensor) -> int:

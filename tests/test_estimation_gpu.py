@@ -217,3 +217,19 @@ def test_vs_fast_dead_tile_skipping_matches_exact(P, s):
     # far-from-diagonal keys: probabilities below fp32's range in both paths
     far = s // 4
     assert float(vsf[:, :far].abs().max()) == 0.0 and float(vse[:, :far].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("n,k,kind", [(1, 1, "rand"), (10, 20, "rand"), (1000, 100, "ties"), (4097, 4097, "ties"),
+                                      (100000, 6096, "rand"), (1 << 20, 16384, "ties"), (5000, 300, "zeros")])
+def test_argtopk_matches_reference_rule(P, n, k, kind):
+    """spf_argtopk == np.argsort(-x, kind="stable")[:k] (estimator.py:59-67): descending
+    values, ties to the lower index, -0.0 equal to +0.0, k clipped to n."""
+    rng = np.random.Generator(np.random.PCG64(n + k))
+    if kind == "rand":
+        x = rng.standard_normal(n)
+    elif kind == "ties":
+        x = rng.integers(0, 50, n).astype(np.float64) / 7.0
+    else:
+        x = np.where(rng.random(n) < 0.5, 0.0, -0.0) + np.where(rng.random(n) < 0.01, 1.0, 0.0)
+    got = P.argtopk(x, k)
+    np.testing.assert_array_equal(got, port.argtopk(x, k))

@@ -35,6 +35,11 @@ def main():
     lse = torch.empty(hq, s, dtype=torch.float32, device=dev)
     kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), 64, lay.tiles, lay.tile_offsets, lay.cols,
                                        lay.col_offsets, lse=lse)
+    # paired-box kernel for the Block-Sparse head, union kernel for the rest (one call)
+    pair = torch.tensor([0, 0, 1, 0], dtype=torch.uint8, device=dev)
+    kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), 64, lay.tiles, lay.tile_offsets, lay.cols,
+                                       lay.col_offsets, pair_heads=pair)
+    P.argtopk(torch.randn(5000, generator=g, device=dev).double().cpu().numpy(), 300)
     qf, kf, vf = (x[:, :1000].float().contiguous() for x in (q, k, v))
     lay32 = P.build_layer_layout(qf, kf, [P.VerticalSlash(32, 128)] * hq, 64)
     kernels.sparse_flash_attention_gpu(qf, kf, vf, 1 / math.sqrt(d), 64, lay32.tiles, lay32.tile_offsets,

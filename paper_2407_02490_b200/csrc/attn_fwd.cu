@@ -74,8 +74,14 @@ constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
-  static constexpr int kK = kSplit ? 2 : 3;
-  static constexpr int kV = 2;
+#ifndef SPF_RING_K
+#define SPF_RING_K 3
+#endif
+#ifndef SPF_RING_V
+#define SPF_RING_V 2
+#endif
+  static constexpr int kK = kSplit ? 2 : SPF_RING_K;
+  static constexpr int kV = kSplit ? 2 : SPF_RING_V;
   static constexpr int kD = 3;  // step descriptors: written with K (one step ahead), freed by the softmax
 };
 

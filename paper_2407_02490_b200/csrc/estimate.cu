@@ -105,6 +105,92 @@ __global__ void __launch_bounds__(kScoreThreads, 2) bs_score_kernel(
   }
 }
 
+// Same scores, same per-element fma order (c ascending), for d % 4 == 0: 128 threads per
+// 64x64 tile of the block-causal triangle only (blockIdx.x enumerates the lower-triangle
+// tiles), 8 rows x 4 columns per thread so the fp64 pipe, not shared memory, is the
+// limit; the staged operands are stored with consecutive rows in consecutive lanes
+// (conflict-free) from 16-byte global loads.
+constexpr int kScore2Threads = 128;
+
+__global__ void __launch_bounds__(kScore2Threads, 4) bs_score_tri_kernel(
+    const float* __restrict__ qp, const float* __restrict__ kp, const int32_t* __restrict__ head_ids,
+    int heads_per_kv, int N, int d, double scale, double* __restrict__ out) {
+  __shared__ __align__(16) double At[kDc * kTile];
+  __shared__ __align__(16) double Bt[kDc * kTile];
+  const int hi = blockIdx.y;
+  const int h = head_ids ? head_ids[hi] : hi;
+  const int kvh = h / heads_per_kv;
+  // lower-triangle tile t -> (at, bt), bt <= at
+  const int t = blockIdx.x;
+  int at = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((at + 1) * (at + 2) / 2 <= t) ++at;
+  while (at * (at + 1) / 2 > t) --at;
+  const int bt = t - at * (at + 1) / 2;
+  const int a0 = at * kTile, b0 = bt * kTile;
+  const float* Ah = qp + (int64_t)h * N * d;
+  const float* Bh = kp + (int64_t)kvh * N * d;
+  const int tid = threadIdx.x, tr = tid >> 4, tk = tid & 15;
+  double acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int c0 = 0; c0 < d; c0 += kDc) {
+    __syncthreads();
+    const int cn = min(kDc, d - c0);
+    for (int e = tid; e < kTile * (kDc / 4); e += kScore2Threads) {
+      const int r = e & (kTile - 1), c4 = (e >> 6) * 4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (c4 < cn) {
+        if (a0 + r < N) a = *reinterpret_cast<const float4*>(Ah + (int64_t)(a0 + r) * d + c0 + c4);
+        if (b0 + r < N) b = *reinterpret_cast<const float4*>(Bh + (int64_t)(b0 + r) * d + c0 + c4);
+      }
+      At[(c4 + 0) * kTile + r] = a.x;
+      At[(c4 + 1) * kTile + r] = a.y;
+      At[(c4 + 2) * kTile + r] = a.z;
+      At[(c4 + 3) * kTile + r] = a.w;
+      Bt[(c4 + 0) * kTile + r] = b.x;
+      Bt[(c4 + 1) * kTile + r] = b.y;
+      Bt[(c4 + 2) * kTile + r] = b.z;
+      Bt[(c4 + 3) * kTile + r] = b.w;
+    }
+    __syncthreads();
+    auto step = [&](int c) {
+      double qv[8], kv[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double2 v = *reinterpret_cast<const double2*>(At + c * kTile + 8 * tr + 2 * m);
+        qv[2 * m] = v.x;
+        qv[2 * m + 1] = v.y;
+      }
+#pragma unroll
+      for (int y = 0; y < 4; ++y) kv[y] = Bt[c * kTile + tk + 16 * y];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[i][y] = fma(qv[i], kv[y], acc[i][y]);
+    };
+    if (cn == kDc) {  // fully unrolled: the shared-memory loads are scheduled ahead of the fmas
+#pragma unroll
+      for (int c = 0; c < kDc; ++c) step(c);
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < cn; ++c) step(c);
+    }
+  }
+  double* outh = out + (int64_t)hi * N * N;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int a = a0 + 8 * tr + i;
+    if (a >= N) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int b = b0 + tk + 16 * y;
+      if (b < N) outh[(int64_t)a * N + b] = (b <= a) ? scale * acc[i][y] : -INFINITY;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- Block-Sparse
 template <typename T>
 __global__ void pool_kernel(const T* __restrict__ x, int64_t n_rows_total, int S, int d, int B,
@@ -125,11 +211,46 @@ __global__ void pool_kernel(const T* __restrict__ x, int64_t n_rows_total, int S
   pooled[idx] = __double2float_rn(acc / (double)(r1 - r0));
 }
 
+// Vectorised pooling: one thread per (head, row block, 16-byte column chunk), the same
+// sequential fp64 sum per column as pool_kernel (identical results); requires
+// d * sizeof(T) % 16 == 0 and a 16-byte aligned base.
+template <typename T>
+__global__ void pool_vec_kernel(const T* __restrict__ x, int64_t n_heads, int S, int d, int B,
+                                float* __restrict__ pooled) {
+  constexpr int kV = 16 / sizeof(T);
+  const int n_blk = (S + B - 1) / B;
+  const int dv = d / kV;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n_heads * (int64_t)n_blk * dv) return;
+  const int cv = (int)(idx % dv);
+  const int64_t hb = idx / dv;
+  const int64_t h = hb / n_blk;
+  const int r = (int)(hb % n_blk);
+  const int r0 = r * B, len = min(B, S - r0);
+  const uint4* base = reinterpret_cast<const uint4*>(x + (h * S + r0) * (int64_t)d) + cv;
+  double acc[kV];
+#pragma unroll
+  for (int j = 0; j < kV; ++j) acc[j] = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < len; ++i) {
+    const uint4 u = __ldcs(base + (int64_t)i * dv);
+    const T* v = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int j = 0; j < kV; ++j) acc[j] += ld_as_double(v + j);
+  }
+  float4* out = reinterpret_cast<float4*>(pooled + hb * d + (int64_t)cv * kV);
+#pragma unroll
+  for (int j = 0; j < kV; j += 4)
+    out[j / 4] = make_float4(__double2float_rn(acc[j] / len), __double2float_rn(acc[j + 1] / len),
+                             __double2float_rn(acc[j + 2] / len), __double2float_rn(acc[j + 3] / len));
+}
+
 constexpr int kBsThreads = 256;
 
 // One CTA per (head, block row r): block-causal softmax of the pooled scores
-// (fp64, rounded to fp32), top-min(k_b, r+1) with the diagonal forced.
-__global__ void __launch_bounds__(kBsThreads) bs_row_kernel(const double* __restrict__ scores, int N, int k_b, int B,
+// (fp64, rounded to fp32), top-min(k_b, r+1) with the diagonal forced.  The row's
+// exponentials overwrite its scores (scratch), so each is evaluated once.
+__global__ void __launch_bounds__(kBsThreads) bs_row_kernel(double* __restrict__ scores, int N, int k_b, int B,
                                                             const int32_t* __restrict__ head_ids,
                                                             const int64_t* __restrict__ tile_offsets,
                                                             int32_t* __restrict__ tile_starts) {
@@ -141,7 +262,7 @@ __global__ void __launch_bounds__(kBsThreads) bs_row_kernel(const double* __rest
   const int h = head_ids ? head_ids[hi] : hi;
   const int r = blockIdx.x;
   const int n = r + 1;
-  const double* sr = scores + ((int64_t)hi * N + r) * N;
+  double* sr = scores + ((int64_t)hi * N + r) * N;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // row max (exact)
   double m = -INFINITY;
@@ -154,13 +275,17 @@ __global__ void __launch_bounds__(kBsThreads) bs_row_kernel(const double* __rest
   __syncthreads();
   // denominator (fixed tree order)
   double l = 0.0;
-  for (int b = tid; b < n; b += kBsThreads) l += exp(sr[b] - m);
+  for (int b = tid; b < n; b += kBsThreads) {  // the exponential is kept in place (same thread reads it back)
+    const double e = exp(sr[b] - m);
+    sr[b] = e;
+    l += e;
+  }
   for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
   if (lane == 0) red[wid] = l;
   __syncthreads();
   l = 0.0;
   for (int w = 0; w < kBsThreads / 32; ++w) l += red[w];
-  for (int b = tid; b < n; b += kBsThreads) pv[b] = __double2float_rn(exp(sr[b] - m) / l);
+  for (int b = tid; b < n; b += kBsThreads) pv[b] = __double2float_rn(sr[b] / l);
   __syncthreads();
   const int64_t row = (int64_t)h * N + r;
   TK::run(sm, pv, n, min(k_b, n), r, false, tile_starts + tile_offsets[row], B);
@@ -182,14 +307,25 @@ int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, cons
   {
     const int64_t tq = (int64_t)Hq * N * d, tk = (int64_t)Hkv * N * d;
     note_launches(3);  // pool q, pool k, row top-k (+1 block scores below)
-    pool_kernel<T><<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
-    pool_kernel<T><<<(unsigned)((tk + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
+    constexpr int kV = 16 / sizeof(T);
+    const bool vec = d % kV == 0 && reinterpret_cast<uintptr_t>(q) % 16 == 0 && reinterpret_cast<uintptr_t>(k) % 16 == 0;
+    if (vec) {
+      pool_vec_kernel<T><<<(unsigned)((tq / kV + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
+      pool_vec_kernel<T><<<(unsigned)((tk / kV + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
+    } else {
+      pool_kernel<T><<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(q, Hq, S, d, B, qp);
+      pool_kernel<T><<<(unsigned)((tk + 255) / 256), 256, 0, st>>>(k, Hkv, S, d, B, kp);
+    }
     if ((rc = check_cuda(cudaGetLastError(), "bs pool"))) return rc;
   }
   const int nt = (N + kTile - 1) / kTile;
   note_launches(1);
-  bs_score_kernel<<<dim3((unsigned)nt, (unsigned)nt, (unsigned)n_heads), kScoreThreads, 0, st>>>(
-      qp, kp, head_ids, Hq / Hkv, N, d, 1.0 / sqrt((double)d), sc);
+  if (d % 4 == 0)
+    bs_score_tri_kernel<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)n_heads), kScore2Threads, 0, st>>>(
+        qp, kp, head_ids, Hq / Hkv, N, d, 1.0 / sqrt((double)d), sc);
+  else
+    bs_score_kernel<<<dim3((unsigned)nt, (unsigned)nt, (unsigned)n_heads), kScoreThreads, 0, st>>>(
+        qp, kp, head_ids, Hq / Hkv, N, d, 1.0 / sqrt((double)d), sc);
   if ((rc = check_cuda(cudaGetLastError(), "bs score"))) return rc;
   const size_t rsmem = (size_t)N * sizeof(float);
   if ((rc = check_cuda(cudaFuncSetAttribute(bs_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem),

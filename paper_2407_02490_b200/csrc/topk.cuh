@@ -8,9 +8,12 @@
 //     `descending` is set, as estimator.py:114 does for slashes).
 //
 // Keys: monotone unsigned images of the float/double values.  Radix select in
-// 11-bit digits finds the exact k-th largest key T and how many T-valued
-// elements are taken (the lowest-index ones); one ordered pass then compacts
-// the selection in index order with block scans.
+// 8-bit digits finds the exact k-th largest key T and how many T-valued
+// elements are taken (the lowest-index ones); once the boundary bucket fits in
+// shared memory its keys are gathered and the remaining rounds count only them.
+// When every T-valued element is taken (no tie straddles the boundary) one
+// ordered pass writes the selection; otherwise warp-cooperative ordered passes
+// rank the T-valued elements by index.
 #pragma once
 #include <cub/block/block_scan.cuh>
 #include <stdint.h>
@@ -37,14 +40,19 @@ struct BlockTopK {
   using Scan = cub::BlockScan<int, kThreads>;
 
   static constexpr int kWarps = kThreads / 32;
+  static constexpr int kCap = 2048;
   struct Storage {
     int hist[kBins];
     typename Scan::TempStorage scan;
     Key prefix;
     int krem;
+    int bcount;  // elements in the bucket chosen by the last radix round
+    int ncand;
     int force_pos;
     int force_sel;
     int wcnt[2][kWarps];  // per-warp T-valued / selected counts (index-ordered passes)
+    int wdrop[kWarps];
+    Key cand[kCap];  // keys of the boundary bucket once it fits (later rounds only count)
   };
 
   // vals: n candidates (global or shared).  Writes k_eff = min(k, n) indices to out.
@@ -54,13 +62,21 @@ struct BlockTopK {
     if (k > n) k = n;
     if (k <= 0) return;
     Key prefix = 0, pmask = 0;
-    int krem = k;
+    int krem = k, bcount = 0;
+    bool listed = false;
     for (int shift = kKeyBits - kBits; shift > -kBits; shift -= kBits) {
       const int sh = shift < 0 ? 0 : shift;
       const int width = shift < 0 ? kBits + shift : kBits;
       const Key dmask = (Key)((1u << width) - 1);
       for (int i = tid; i < kBins; i += kThreads) sm.hist[i] = 0;
       __syncthreads();
+      if (listed) {  // the boundary bucket's keys are in sm.cand
+        const int nc = sm.ncand;
+        for (int j = tid; j < nc; j += kThreads) {
+          const Key key = sm.cand[j];
+          if ((key & pmask) == prefix) atomicAdd(&sm.hist[(int)((key >> sh) & dmask)], 1);
+        }
+      } else
       // warp-aggregated histogram: the leading digits are highly concentrated (values of one
       // exponent), so lanes with equal digits are merged before the shared-memory atomic
       for (int base = 0; base < n; base += kThreads) {
@@ -104,13 +120,40 @@ struct BlockTopK {
           const int digit = kBins - 1 - (tid * kPer + j);
           sm.prefix = prefix | ((Key)digit << sh);
           sm.krem = krem - before;
+          sm.bcount = local[j];
         }
       }
       __syncthreads();
       prefix = sm.prefix;
       krem = sm.krem;
+      bcount = sm.bcount;
       pmask |= dmask << sh;
       __syncthreads();
+      if (!listed && shift - kBits > -kBits && bcount <= kCap) {
+        // one pass gathers the bucket's keys; the remaining rounds scan only them
+        if (tid == 0) sm.ncand = 0;
+        __syncthreads();
+        const int lane = tid & 31;
+        for (int base = 0; base < n; base += kThreads) {
+          const int i = base + tid;
+          Key key = 0;
+          bool hit = false;
+          if (i < n) {
+            key = mono_key(vals[i]);
+            hit = (key & pmask) == prefix;
+          }
+          const unsigned hm = __ballot_sync(0xffffffffu, hit);
+          if (hm) {
+            const int lead = __ffs(hm) - 1;
+            int wb = 0;
+            if (lane == lead) wb = atomicAdd(&sm.ncand, __popc(hm));
+            wb = __shfl_sync(0xffffffffu, wb, lead);
+            if (hit) sm.cand[wb + __popc(hm & ((1u << lane) - 1u))] = key;
+          }
+        }
+        __syncthreads();
+        listed = true;
+      }
     }
     const Key thr = prefix;  // exact k-th largest key; krem T-valued elements are taken
     // Index-ordered passes, warp-cooperative: warp w owns a contiguous range of 32-element
@@ -120,6 +163,48 @@ struct BlockTopK {
     const unsigned lt = (1u << lane) - 1u;
     const int wchunk = (((n + kWarps - 1) / kWarps) + 31) & ~31;
     const int w0 = min(n, w * wchunk), w1 = min(n, w0 + wchunk);
+    if (bcount == krem) {
+      // Every T-valued element is taken (no tie straddles the boundary): selected = key >= T.
+      // If force_idx is not among them it replaces the weakest pick, the T-valued element of
+      // highest index; the selection is then written in index order in one pass.
+      const bool need_force = force_idx >= 0 && force_idx < n && mono_key(vals[force_idx]) < thr;
+      int selc = 0, drop = -1;
+      for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        const Key key = i < w1 ? mono_key(vals[i]) : (Key)0;
+        selc += __popc(__ballot_sync(0xffffffffu, i < w1 && key >= thr));
+        if (need_force) {
+          const unsigned em = __ballot_sync(0xffffffffu, i < w1 && key == thr);
+          if (em) drop = base + 31 - __clz(em);
+        }
+      }
+      if (lane == 0) {
+        sm.wcnt[1][w] = selc;
+        sm.wdrop[w] = drop;
+      }
+      __syncthreads();
+      int pos = 0;
+      for (int x = 0; x < w; ++x) pos += sm.wcnt[1][x];
+      int idx_drop = -1;
+      if (need_force) {
+        for (int x = 0; x < kWarps; ++x) idx_drop = max(idx_drop, sm.wdrop[x]);
+        pos += (force_idx < w0 ? 1 : 0) - (idx_drop < w0 ? 1 : 0);
+      }
+      for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        const Key key = i < w1 ? mono_key(vals[i]) : (Key)0;
+        bool s = i < w1 && key >= thr;
+        if (need_force) s = (s && i != idx_drop) || (i < w1 && i == force_idx);
+        const unsigned smask = __ballot_sync(0xffffffffu, s);
+        if (s) {
+          const int slot = pos + __popc(smask & lt);
+          out[descending ? (k - 1 - slot) : slot] = i * out_scale;
+        }
+        pos += __popc(smask);
+      }
+      __syncthreads();
+      return;
+    }
     // pass A: T-valued count per warp
     int eqc = 0;
     for (int base = w0; base < w1; base += 32) {

@@ -1,6 +1,7 @@
 """A/B timing of two libspf builds on the same inputs, interleaved (attention only).
 
     python benchmarks/ab_attention.py A/libspf.so B/libspf.so     # AB_CFG=vs|bs|as AB_SEQ=131072 AB_REPS=12
+    AB_HQ=56 AB_GEN=iid AB_PAIR=1 AB_CFG=bs AB_SEQ=262144 ...       # the C4 layer through the paired-box kernel
 
 Both libraries are loaded side by side with ctypes and launched alternately on one
 C2-shaped layer (32 q-heads, 8 kv, d=128, G-local), so clock and power drift hit
@@ -10,23 +11,28 @@ import ctypes, os, statistics, sys
 sys.path.insert(0, os.getcwd())
 import torch
 import paper_2407_02490_b200 as P
-from benchmarks.workloads import g_local_qkv
+from benchmarks.workloads import g_iid_qkv, g_local_qkv
 libs = [ctypes.CDLL(os.path.abspath(p)) for p in sys.argv[1:3]]
 seq = int(os.environ.get("AB_SEQ", "131072"))
-q, k, v = g_local_qkv(32, 8, seq, 128, seed=0, device="cuda")
+hq = int(os.environ.get("AB_HQ", "32"))
+gen = g_iid_qkv if os.environ.get("AB_GEN", "local") == "iid" else g_local_qkv
+q, k, v = gen(hq, 8, seq, 128, seed=0, device="cuda")
 cfg = os.environ.get("AB_CFG", "vs")
-cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * 32, "bs": [P.BlockSparse(100)] * 32, "as": [P.AShape(128, 4096)] * 32,
-        "tiny": [P.AShape(1, 64)] * 32, "small": [P.AShape(64, 640)] * 32}[cfg]
+cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * hq, "bs": [P.BlockSparse(100)] * hq, "as": [P.AShape(128, 4096)] * hq,
+        "tiny": [P.AShape(1, 64)] * hq, "small": [P.AShape(64, 640)] * hq}[cfg]
+pair = torch.full((hq,), int(os.environ.get("AB_PAIR", "0")), dtype=torch.uint8, device="cuda")
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p
 def run(lib):
-    lib.spf_sparse_flash_rows.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                          ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
-    rc = lib.spf_sparse_flash_rows(0, vp(q.data_ptr()), vp(k.data_ptr()), vp(v.data_ptr()), 32, 8, seq, 128,
-                                   ctypes.c_float(128 ** -0.5), 64, vp(lay.tiles.data_ptr()), vp(lay.tile_offsets.data_ptr()),
-                                   vp(lay.cols.data_ptr() if lay.cols.numel() else 0), vp(lay.col_offsets.data_ptr()),
-                                   vp(out.data_ptr()), None, 0, vp(torch.cuda.current_stream().cuda_stream))
+    lib.spf_sparse_flash_rows_ex.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp,
+                                             vp, ctypes.c_size_t, vp]
+    rc = lib.spf_sparse_flash_rows_ex(0, vp(q.data_ptr()), vp(k.data_ptr()), vp(v.data_ptr()), hq, 8, seq, 128,
+                                      ctypes.c_float(128 ** -0.5), 64, vp(lay.tiles.data_ptr()),
+                                      vp(lay.tile_offsets.data_ptr()), vp(lay.cols.data_ptr() if lay.cols.numel() else 0),
+                                      vp(lay.col_offsets.data_ptr()), vp(pair.data_ptr()), vp(out.data_ptr()), None,
+                                      None, 0, vp(torch.cuda.current_stream().cuda_stream))
     assert rc == 0
 ts = [[], []]
 for r in range(int(os.environ.get("AB_REPS", "12"))):

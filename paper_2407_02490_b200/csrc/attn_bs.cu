@@ -94,12 +94,16 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // work item: heavy (late) row tiles first, heads fastest; only the paired heads
+  // work item: kv-head major, then heavy (late) row tiles first, the group's q-heads fastest.
+  // Block-Sparse tiles are scattered over the whole causal prefix, so the CTAs in flight
+  // should share one kv head's K/V (<= 2 * S * d * 2 bytes) in L2 rather than all of them.
   const int item = blockIdx.x;
-  const int ct = n_ctile - 1 - item / p.Hq;
-  const int h = item % p.Hq;
+  const int hpk = p.Hq / p.Hkv;
+  const int kvh = item / (n_ctile * hpk);
+  const int rem = item - kvh * (n_ctile * hpk);
+  const int ct = n_ctile - 1 - rem / hpk;
+  const int h = kvh * hpk + rem % hpk;
   if (p.pair_heads == nullptr || p.pair_heads[h] == 0) return;  // the union kernel's head
-  const int kvh = h / (p.Hq / p.Hkv);
   const int S = p.S;
   const int n_rows = (S + kBox - 1) / kBox;
   const int R0 = ct * kRows;

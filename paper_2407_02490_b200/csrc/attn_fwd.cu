@@ -74,6 +74,9 @@ constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
+#ifndef SPF_KV_MAJOR
+#define SPF_KV_MAJOR 0  // kv-head-major item order: 0.7-1.1 % slower on C2-shaped VS / A-shape layers
+#endif
 #ifndef SPF_RING_K
 #define SPF_RING_K 3
 #endif
@@ -188,13 +191,22 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- work item: heavy (late) row tiles first, heads fastest --------------------
+  // ---- work item: heavy (late) row tiles first, heads fastest (SPF_KV_MAJOR: kv-head major,
+  // as the paired-box kernel does for the scattered Block-Sparse tiles) ---------------------
   int item = blockIdx.x;
   if (p.work_order != nullptr) item = p.work_order[item];
+#if SPF_KV_MAJOR
+  const int hpk = p.Hq / p.Hkv;
+  const int kvh = item / (n_ctile * hpk);
+  const int rem = item - kvh * (n_ctile * hpk);
+  const int ct = n_ctile - 1 - rem / hpk;
+  const int h = kvh * hpk + rem % hpk;
+#else
   const int ct = n_ctile - 1 - item / p.Hq;
   const int h = item % p.Hq;
-  if (p.pair_heads != nullptr && p.pair_heads[h]) return;  // run by the paired-box kernel (attn_bs.cu)
   const int kvh = h / (p.Hq / p.Hkv);
+#endif
+  if (p.pair_heads != nullptr && p.pair_heads[h]) return;  // run by the paired-box kernel (attn_bs.cu)
   const int S = p.S, B = p.B;
   const int n_rows = (S + B - 1) / B;
   const int R0 = ct * kRows;

@@ -20,18 +20,19 @@ q, k, v = gen(hq, 8, seq, 128, seed=0, device="cuda")
 cfg = os.environ.get("AB_CFG", "vs")
 cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * hq, "bs": [P.BlockSparse(100)] * hq, "as": [P.AShape(128, 4096)] * hq,
         "tiny": [P.AShape(1, 64)] * hq, "small": [P.AShape(64, 640)] * hq}[cfg]
-pair = torch.full((hq,), int(os.environ.get("AB_PAIR", "0")), dtype=torch.uint8, device="cuda")
+pair = torch.arange(hq, dtype=torch.int32, device="cuda")  # AB_PAIR=1: every head through the paired-box kernel
+n_pair = hq if os.environ.get("AB_PAIR", "0") == "1" else 0
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p
 def run(lib):
     lib.spf_sparse_flash_rows_ex.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                             ctypes.c_int, ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp,
-                                             vp, ctypes.c_size_t, vp]
+                                             ctypes.c_int, ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp,
+                                             ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp]
     rc = lib.spf_sparse_flash_rows_ex(0, vp(q.data_ptr()), vp(k.data_ptr()), vp(v.data_ptr()), hq, 8, seq, 128,
                                       ctypes.c_float(128 ** -0.5), 64, vp(lay.tiles.data_ptr()),
                                       vp(lay.tile_offsets.data_ptr()), vp(lay.cols.data_ptr() if lay.cols.numel() else 0),
-                                      vp(lay.col_offsets.data_ptr()), vp(pair.data_ptr()), vp(out.data_ptr()), None,
+                                      vp(lay.col_offsets.data_ptr()), vp(pair.data_ptr()), n_pair, vp(out.data_ptr()), None,
                                       None, 0, vp(torch.cuda.current_stream().cuda_stream))
     assert rc == 0
 ts = [[], []]

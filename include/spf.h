@@ -74,17 +74,19 @@ int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const voi
                               int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                               const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
                               void* out, float* lse_out, void* workspace, size_t workspace_bytes, void* stream);
-/* Same, with a per-head routing hint: pair_heads (device uint8 [n_q_heads], may be
- * NULL) marks heads whose 64-row blocks have no residual columns and rarely share
- * tiles -- the Block-Sparse heads of estimator.estimate_block_sparse
- * (estimator.py:117-143) -- which then run the paired-box kernel: one step pairs the
- * next tile of each of a CTA's two row blocks (bf16, block_size 64, head_dim <= 128;
- * otherwise the hint is ignored).  Results follow the same contract. */
+/* Same, with a per-head routing hint: pair_heads (device int32 [n_pair_heads], distinct
+ * q-head ids in [0, n_q_heads); NULL when n_pair_heads == 0) lists heads whose 64-row
+ * blocks have no residual columns and rarely share tiles -- the Block-Sparse heads of
+ * estimator.estimate_block_sparse (estimator.py:117-143) -- which then run the
+ * paired-box kernel: one step pairs the next tile of each of a CTA's two row blocks
+ * (bf16, block_size 64, head_dim <= 128; otherwise the hint is ignored).  The count is
+ * a host value, so a layer whose heads are all listed launches only that kernel.
+ * Results follow the same contract. */
 int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
-                             const uint8_t* pair_heads, void* out, float* lse_out, void* workspace,
-                             size_t workspace_bytes, void* stream);
+                             const int32_t* pair_heads, int n_pair_heads, void* out, float* lse_out,
+                             void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * argtopk (estimator.py:59-67): indices of the k largest values in descending-value

@@ -35,7 +35,7 @@ SIGNATURES = {
     "spf_sparse_flash_rows_lse": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
                                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
     "spf_sparse_flash_rows_ex": (_c_int, [_c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_float, _c_int,
-                                          _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp]),
+                                          _vp, _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_size, _vp]),
     "spf_argtopk_workspace_size": (_c_size, [_i64]),
     "spf_argtopk": (_c_int, [_vp, _i64, _c_int, _vp, _vp, _c_size, _vp]),
     "spf_vs_estimate_workspace_size": (_c_size, [_c_int] * 8),

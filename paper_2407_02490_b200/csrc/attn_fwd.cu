@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   const int h = item % p.Hq;
   const int kvh = h / (p.Hq / p.Hkv);
 #endif
-  if (p.pair_heads != nullptr && p.pair_heads[h]) return;  // run by the paired-box kernel (attn_bs.cu)
+  for (int i = 0; i < p.n_pair; ++i)
+    if (p.pair_heads[i] == h) return;  // run by the paired-box kernel (attn_bs.cu)
   const int S = p.S, B = p.B;
   const int n_rows = (S + B - 1) / B;
   const int R0 = ct * kRows;

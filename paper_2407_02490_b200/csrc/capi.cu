@@ -129,15 +129,15 @@ int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const voi
                               const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
                               void* out, float* lse_out, void* workspace, size_t workspace_bytes, void* stream) {
   return spf_sparse_flash_rows_ex(dtype, q, k, v, n_q_heads, n_kv_heads, seq_len, head_dim, scale, block_size,
-                                  tile_starts, tile_offsets, col_indices, col_offsets, nullptr, out, lse_out,
+                                  tile_starts, tile_offsets, col_indices, col_offsets, nullptr, 0, out, lse_out,
                                   workspace, workspace_bytes, stream);
 }
 
 int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
-                             const uint8_t* pair_heads, void* out, float* lse_out, void* workspace,
-                             size_t workspace_bytes, void* stream) {
+                             const int32_t* pair_heads, int n_pair_heads, void* out, float* lse_out,
+                             void* workspace, size_t workspace_bytes, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype != SPF_DTYPE_BF16 && dtype != SPF_DTYPE_F32) return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
   if (seq_len < 1 || head_dim < 1 || n_q_heads < 1 || n_kv_heads < 1)
@@ -168,6 +168,9 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
   a.n_work = 0;
   a.lse = lse_out;
   a.pair_heads = nullptr;
+  a.n_pair = 0;
+  if (n_pair_heads < 0 || n_pair_heads > n_q_heads || (n_pair_heads > 0 && pair_heads == nullptr))
+    return set_error(SPF_ERR_INVALID, "bad pair head list (%d heads)", n_pair_heads);
   const size_t need = spf_sparse_flash_workspace_size(dtype, n_q_heads, n_kv_heads, seq_len, head_dim);
   if (need == 0) {
     a.q_hi = q;
@@ -210,10 +213,13 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
     a.k_lo = kl;
     a.v_lo = vl;
   }
-  if (pair_heads != nullptr && attn_pair_supported(a)) {
+  if (n_pair_heads > 0 && attn_pair_supported(a)) {
     a.pair_heads = pair_heads;
-    int rc = launch_sparse_attn(a, st);  // the other heads
-    if (rc) return rc;
+    a.n_pair = n_pair_heads;
+    if (n_pair_heads < n_q_heads) {
+      const int rc = launch_sparse_attn(a, st);  // the other heads
+      if (rc) return rc;
+    }
     return launch_sparse_attn_pairs(a, st);
   }
   return launch_sparse_attn(a, st);

@@ -34,7 +34,8 @@ struct AttnArgs {
   const int32_t* work_order;  // optional: CTA -> work-item list (nullptr = all items, heavy rows first)
   int n_work;                 // number of entries in work_order
   float* lse;                 // optional [Hq][S]: natural-log sum of exp(scale * q.k) over the row's cells
-  const uint8_t* pair_heads;  // optional [Hq]: 1 = run with the paired-box kernel (attn_bs.cu)
+  const int32_t* pair_heads;  // optional device list of q-heads run by the paired-box kernel (attn_bs.cu)
+  int n_pair;
 };
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);

@@ -38,6 +38,25 @@ def _flatten(per_row, n_rows: int):
     return flat, off
 
 
+def _pair_list(pair_heads, hq: int, dev) -> torch.Tensor | None:
+    """Device int32 list of the paired-box kernel's heads (see sparse_flash_attention_gpu)."""
+    if pair_heads is None:
+        return None
+    if not isinstance(pair_heads, torch.Tensor):
+        pair_heads = torch.as_tensor(pair_heads)
+    if pair_heads.dtype in (torch.bool, torch.uint8):
+        if pair_heads.numel() != hq:
+            raise ValueError("a pair_heads mask must have one entry per q-head")
+        pair_heads = torch.nonzero(pair_heads.reshape(-1)).reshape(-1)
+    elif pair_heads.dtype not in (torch.int32, torch.int64):
+        raise ValueError("pair_heads must be a head-id list or a bool/uint8 mask")
+    if pair_heads.numel() == 0:
+        return None
+    if pair_heads.numel() > hq:
+        raise ValueError("more pair heads than q-heads")
+    return pair_heads.to(device=dev, dtype=torch.int32).contiguous()
+
+
 def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float, block_size: int,
                                tile_starts: torch.Tensor, tile_offsets: torch.Tensor, col_indices: torch.Tensor,
                                col_offsets: torch.Tensor, out: torch.Tensor | None = None,
@@ -50,9 +69,11 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     CSR over (head, row): offsets int64 [Hq*n_rows+1], entries int32.
     Returns out [Hq, S, d] in the input dtype.  ``lse`` (optional fp32 [Hq, S])
     receives each row's natural-log sum of exp(scale * q.k) over its cells.
-    ``pair_heads`` (optional uint8 [Hq] on the device) marks heads without residual
-    columns whose row blocks rarely share tiles (Block-Sparse heads): they run the
-    paired-box kernel (include/spf.h, spf_sparse_flash_rows_ex).
+    ``pair_heads`` (optional) names the heads without residual columns whose row
+    blocks rarely share tiles (Block-Sparse heads): they run the paired-box kernel
+    (include/spf.h, spf_sparse_flash_rows_ex).  Either a device int32 tensor of
+    distinct head ids (the hot path: its length is host metadata, no sync), or a bool /
+    uint8 [Hq] mask (converted here).
     """
     dev = _dev.require_cuda(q.device)
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
@@ -77,12 +98,11 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     cs = col_indices if col_indices.numel() else None
     if lse is not None and (lse.dtype != torch.float32 or lse.numel() != hq * s_len or not lse.is_contiguous()):
         raise ValueError("lse must be a contiguous fp32 [Hq, S] tensor")
-    if pair_heads is not None and (pair_heads.dtype != torch.uint8 or pair_heads.numel() != hq):
-        raise ValueError("pair_heads must be a uint8 [Hq] tensor")
+    pair_list = _pair_list(pair_heads, hq, dev)
     _lib.check(lib.spf_sparse_flash_rows_ex(
         dtype, _dev.ptr(q), _dev.ptr(k), _dev.ptr(v), hq, hkv, s_len, d, float(scale), int(block_size),
-        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(pair_heads),
-        _dev.ptr(out), _dev.ptr(lse), _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows_ex")
+        _dev.ptr(ts), _dev.ptr(tile_offsets), _dev.ptr(cs), _dev.ptr(col_offsets), _dev.ptr(pair_list),
+        0 if pair_list is None else int(pair_list.numel()), _dev.ptr(out), _dev.ptr(lse), _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)), "spf_sparse_flash_rows_ex")
     return out
 
 

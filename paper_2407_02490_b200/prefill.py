@@ -127,14 +127,14 @@ _PAIR_CACHE: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
 
 
 def _pair_heads(head_cfgs, device):
-    """uint8 [Hq] mask of the Block-Sparse heads (no residual columns, row blocks that
+    """Device int32 list of the Block-Sparse heads (no residual columns, row blocks that
     rarely share tiles): the attention runs them with the paired-box kernel."""
     key = (str(device), tuple(isinstance(c, BlockSparse) for c in head_cfgs))
     if not any(key[1]):
         return None
     m = _PAIR_CACHE.get(key)
     if m is None:
-        m = torch.tensor(key[1], dtype=torch.uint8, device=device)
+        m = torch.tensor([h for h, bs in enumerate(key[1]) if bs], dtype=torch.int32, device=device)
         _PAIR_CACHE[key] = m
         if len(_PAIR_CACHE) > 64:
             _PAIR_CACHE.popitem(last=False)

@@ -144,12 +144,14 @@ def test_multihead_bf16_gqa(K, s, hq, hkv, b):
     assert worst <= BF16_TOL, worst
 
 
-@pytest.mark.parametrize("s,kb,d", [(1000, 3, 128), (4097, 8, 128), (63, 2, 64), (3000, 1, 64)])
-def test_paired_box_kernel_matches_oracle(K, s, kb, d):
+@pytest.mark.parametrize("s,kb,d,routing", [(1000, 3, 128, "mask"), (4097, 8, 128, "mask"), (63, 2, 64, "mask"),
+                                            (3000, 1, 64, "mask"), (1000, 3, 128, "list"), (4097, 8, 64, "all")])
+def test_paired_box_kernel_matches_oracle(K, s, kb, d, routing):
     """The paired-box kernel (Block-Sparse heads, pair_heads) on block-sparse layouts with
     an odd number of row blocks, rows shorter than k_b, k_b = 1 (diagonal only) and a
-    sub-block sequence: every row equals the oracle kernel; unflagged heads in the same
-    launch still run the union kernel."""
+    sub-block sequence: every row equals the oracle kernel; unlisted heads in the same
+    launch still run the union kernel.  Routing given as a uint8 mask, as an unordered
+    int32 head list, or as every head (then the union kernel is not launched at all)."""
     hq, hkv, b = 4, 2, 64
     rng = np.random.Generator(np.random.PCG64(s + kb))
     q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
@@ -167,7 +169,9 @@ def test_paired_box_kernel_matches_oracle(K, s, kb, d):
     ts, to = port.flatten(tiles_all)
     co = np.zeros(hq * n + 1, np.int64)
     dev = torch.device("cuda")
-    pair = torch.tensor([1, 0, 1, 1], dtype=torch.uint8, device=dev)
+    pair = {"mask": torch.tensor([1, 0, 1, 1], dtype=torch.uint8, device=dev),
+            "list": torch.tensor([3, 0, 2], dtype=torch.int32, device=dev),
+            "all": torch.arange(hq, dtype=torch.int32, device=dev)}[routing]
     args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
             torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
             torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
@@ -182,3 +186,20 @@ def test_paired_box_kernel_matches_oracle(K, s, kb, d):
                                       np.zeros(0, np.int64), np.zeros(n + 1, np.int64))
         assert np.abs(got[h] - want).max() < BF16_TOL, (h, np.abs(got[h] - want).max())
         assert np.abs(got[h] - union[h]).max() < BF16_TOL
+
+
+def test_pair_heads_validation(K):
+    dev = torch.device("cuda")
+    q = torch.zeros(2, 128, 64, dtype=torch.bfloat16, device=dev)
+    k = torch.zeros(1, 128, 64, dtype=torch.bfloat16, device=dev)
+    to = torch.zeros(5, dtype=torch.int64, device=dev)
+    args = (q, k, k, 0.125, 64, torch.zeros(0, dtype=torch.int32, device=dev), to,
+            torch.zeros(0, dtype=torch.int32, device=dev), to)
+    with pytest.raises(ValueError):
+        K.sparse_flash_attention_gpu(*args, pair_heads=torch.ones(3, dtype=torch.uint8, device=dev))
+    with pytest.raises(ValueError):
+        K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(3, dtype=torch.int32, device=dev))
+    with pytest.raises(ValueError):
+        K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.float32, device=dev))
+    out = K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.uint8, device=dev))
+    assert out.abs().max().item() == 0  # no coverage -> zero rows; empty list = union kernel only

@@ -152,16 +152,29 @@ def metric_name(args, cfg) -> str:
     return f"pre-fill attention latency (ms), {cfg['workload']}"
 
 
-def union_steps(tiles_np, toff_np, n_rows, hq):
-    """Kernel steps of the 128-row CTAs: |tiles(2p) U tiles(2p+1)| per pair."""
+def union_steps(tiles_np, toff_np, n_rows, hq, paired=None):
+    """Kernel steps of the 128-row CTAs: |tiles(2p) U tiles(2p+1)| per pair of row blocks
+    (union kernel), or max(n(2p), n(2p+1)) for the heads in ``paired`` (paired-box
+    kernel).  Returns (union steps, paired steps)."""
     import numpy as np
 
     counts = np.diff(toff_np)
     rows = np.repeat(np.arange(hq * n_rows, dtype=np.int64), counts)
     head = rows // n_rows
+    is_pair = np.zeros(hq, dtype=bool)
+    if paired is not None:
+        is_pair[np.asarray(paired, dtype=np.int64)] = True
+    keep = ~is_pair[head]
     pair = head * ((n_rows + 1) // 2) + (rows % n_rows) // 2
-    keys = pair * (np.int64(1) << 32) + tiles_np.astype(np.int64)
-    return int(np.unique(keys).size)
+    keys = pair[keep] * (np.int64(1) << 32) + tiles_np.astype(np.int64)[keep]
+    n_union = int(np.unique(keys).size)
+    n_paired = 0
+    for h in np.nonzero(is_pair)[0]:
+        c = counts[h * n_rows:(h + 1) * n_rows]
+        if n_rows % 2:
+            c = np.append(c, 0)
+        n_paired += int(np.maximum(c[0::2], c[1::2]).sum())
+    return n_union, n_paired
 
 
 def main():
@@ -261,7 +274,7 @@ def main():
     step()
     torch.cuda.synchronize()
     n_rows = (S + B - 1) // B
-    tiles_tot = chips_tot = union_tot = 0
+    tiles_tot = chips_tot = union_tot = paired_tot = 0
     area_tot = 0
     pattern_counts = {}
     for layer in range(L):
@@ -269,7 +282,11 @@ def main():
         tiles_tot += lay.n_tiles
         chips_tot += lay.chips()
         area_tot += int(lay.area().sum().item())
-        union_tot += union_steps(lay.tiles.cpu().numpy(), lay.tile_offsets.cpu().numpy(), n_rows, hq_loc)
+        plist = pair_masks[layer]
+        nu, npr = union_steps(lay.tiles.cpu().numpy(), lay.tile_offsets.cpu().numpy(), n_rows, hq_loc,
+                              None if plist is None else plist.cpu().numpy())
+        union_tot += nu
+        paired_tot += npr
         for c in cfgs[layer]:
             pattern_counts[type(c).__name__] = pattern_counts.get(type(c).__name__, 0) + 1
     for _ in range(args.warmup - 1):
@@ -306,7 +323,8 @@ def main():
     tile_flops = TILE_FLOPS_PER_CELL * D * B * B
     flops_issued_layer = tile_flops * (tiles_tot + chips_tot) / L      # reference-layout algorithmic FLOPs
     achieved_tf = flops_issued_layer / (attn_avg * 1e-3) / 1e12
-    mma_flops_layer = 2 * tile_flops * (union_tot + chips_tot) / L     # what the M=128 CTAs issue
+    # what the M=128 CTAs issue: union step = M128xN64 QK + K64 PV; paired step = N128 QK + K128 PV
+    mma_flops_layer = (2 * tile_flops * (union_tot + chips_tot) + 4 * tile_flops * paired_tot) / L
     traffic = None
     tpath = os.path.join(REPO, "profiles", "attn_traffic.json")
     if os.path.exists(tpath):
@@ -317,7 +335,9 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": tf_sust, "unit": "TFLOP/s",
                 "frac": round(achieved_tf / tf_sust, 4), "traffic": traffic,
-                "kernel": "sparse_attn_fwd_kernel<128,false>", "peak_source": f"{peak_src} bf16 sustained",
+                "kernel": ("sparse_attn_pair_kernel<128>" if union_tot + chips_tot == 0 else
+                           "sparse_attn_fwd_kernel<128,false>" + (" + sparse_attn_pair_kernel<128>" if paired_tot else "")),
+                "peak_source": f"{peak_src} bf16 sustained",
                 "flops_per_launch": flops_issued_layer, "avg_launch_ms": round(attn_avg, 4),
                 "mma_flops_per_launch": mma_flops_layer,
                 "mma_frac": round(mma_flops_layer / (attn_avg * 1e-3) / 1e12 / tf_sust, 4),
@@ -353,7 +373,7 @@ def main():
                        "parallelism": f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
                                       f"divides {HKV}), no data-path collective",
                        "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
-                       "union_steps": union_tot, "output_all_gather": bool(args.gather and world > 1)},
+                       "union_steps": union_tot, "paired_steps": paired_tot, "output_all_gather": bool(args.gather and world > 1)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

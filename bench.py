@@ -189,6 +189,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--shard", default="contiguous", choices=["contiguous", "lpt"],
+                    help="q-head partition over ranks: contiguous kv-group ranges, or LPT on modeled kernel FLOPs")
     ap.add_argument("--gather", action="store_true",
                     help="all-gather every layer's per-rank outputs into the full [Hq, S, d] on every rank "
                          "(the optional collective of SURVEY 8e), inside the timed step")
@@ -223,13 +225,21 @@ def main():
     if world > 1:
         dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     S, HQ, HKV, L, D, B = cfg["seq_len"], cfg["hq"], cfg["hkv"], cfg["layers"], 128, 64
-    from paper_2407_02490_b200.sharding import max_over_ranks, shard_heads
+    from paper_2407_02490_b200.sharding import max_over_ranks, plan_heads_lpt, shard_heads
 
-    shard = shard_heads(HQ, HKV, world, rank)
-    hq_loc = shard.n_q
-    q0 = shard.q_begin
     all_cfgs = layer_configs(cfg)[:L]
-    cfgs = [row[q0:q0 + hq_loc] for row in all_cfgs]
+    if args.shard == "lpt":  # whole kv groups (or heads) balanced on the patterns' modeled kernel FLOPs
+        from paper_2407_02490_b200.patterns import flops_in_kernel
+
+        head_costs = [sum(flops_in_kernel(all_cfgs[layer][h], S, D, B) for layer in range(L)) for h in range(HQ)]
+        shards = [plan_heads_lpt(head_costs, HKV, world, r) for r in range(world)]
+    else:
+        shards = [shard_heads(HQ, HKV, world, r) for r in range(world)]
+    shard = shards[rank]
+    hq_loc = shard.n_q
+    q_idx = torch.tensor(shard.q_heads, dtype=torch.long, device=dev)
+    kv_idx = torch.tensor(shard.kv_stack, dtype=torch.long, device=dev)
+    cfgs = [[row[h] for h in shard.q_heads] for row in all_cfgs]
     from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
 
     table = PatternTable(cfgs)  # this rank's heads; device head groups cached per layer
@@ -239,9 +249,9 @@ def main():
     Q, K, V = [], [], []
     for layer in range(L):
         q, k, v = gen(HQ, HKV, S, D, seed=1000 * layer, device=dev)
-        Q.append(q[q0:q0 + hq_loc].contiguous())
-        K.append(k[shard.kv_begin:shard.kv_end].contiguous())
-        V.append(v[shard.kv_begin:shard.kv_end].contiguous())
+        Q.append(q.index_select(0, q_idx))
+        K.append(k.index_select(0, kv_idx))
+        V.append(v.index_select(0, kv_idx))
         del q, k, v
     out = torch.empty((hq_loc, S, D), dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream()
@@ -251,7 +261,6 @@ def main():
     attn_events = []
     from paper_2407_02490_b200.sharding import gather_heads
 
-    shards = [shard_heads(HQ, HKV, world, r) for r in range(world)]
     from paper_2407_02490_b200.prefill import _pair_heads
 
     pair_masks = [_pair_heads(cfgs[layer], dev) for layer in range(L)]  # Block-Sparse heads: paired-box kernel
@@ -370,8 +379,10 @@ def main():
                        "pattern_heads_this_rank": pattern_counts, "inputs": cfg["inputs"] + " (SURVEY.md 8d)",
                        "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush" % (
                            sum(t.numel() * 2 for t in Q + K + V) / 1e9),
-                       "parallelism": f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
-                                      f"divides {HKV}), no data-path collective",
+                       "parallelism": (f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
+                                       f"divides {HKV}), no data-path collective" if args.shard == "contiguous" else
+                                       f"q-heads sharded over {world} GPU(s) by LPT on modeled kernel FLOPs (whole kv "
+                                       f"groups when {world} <= {HKV}), no data-path collective"),
                        "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
                        "union_steps": union_tot, "paired_steps": paired_tot, "output_all_gather": bool(args.gather and world > 1)},
             "roofline": roofline,

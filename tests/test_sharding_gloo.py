@@ -12,7 +12,17 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2407_02490_b200.sharding import shard_heads
+from paper_2407_02490_b200.sharding import lpt_assign, plan_heads_lpt, shard_heads
+
+
+def _check_kernel_map(s, qpk):
+    """The kernels' GQA map over the rank's stacked K/V reads each head's own kv head."""
+    stack = s.kv_stack
+    ratio = s.n_q // len(stack)
+    assert ratio * len(stack) == s.n_q
+    for i, h in enumerate(s.q_heads):
+        assert stack[i // ratio] == h // qpk
+        assert s.local_kv_index(h) == i // ratio
 
 
 def test_shards_partition_heads():
@@ -21,17 +31,44 @@ def test_shards_partition_heads():
             if world > hq:
                 continue
             shards = [shard_heads(hq, hkv, world, r) for r in range(world)]
-            owned = [h for s in shards for h in range(s.q_begin, s.q_end)]
+            owned = [h for s in shards for h in s.q_heads]
             assert owned == list(range(hq)), (hq, hkv, world)
             sizes = [s.n_q for s in shards]
             assert max(sizes) - min(sizes) <= (hq // hkv if hkv % world == 0 else 1)
             for s in shards:
-                for h in range(s.q_begin, s.q_end):
-                    assert 0 <= s.local_kv_index(h) < s.n_kv
+                _check_kernel_map(s, hq // hkv)
                 if hkv % world == 0:  # whole kv groups: no K/V duplication
-                    assert s.n_q == s.n_kv * (hq // hkv)
+                    assert s.n_q == s.n_kv * (hq // hkv) and s.kv_stack == s.kv_heads
+    # Qwen2 28/4 on 8 GPUs: rank 1 holds q-heads 4..7 = three of group 0 and one of group 1,
+    # so its K/V stack has one entry per q-head
+    s = shard_heads(28, 4, 8, 1)
+    assert s.q_heads == (4, 5, 6, 7) and s.kv_stack == (0, 0, 0, 1)
     with pytest.raises(ValueError):
         shard_heads(6, 4, 2, 0)
+
+
+def test_lpt_plans():
+    # 5 -> r0, 4 -> r1, 3 -> r1 (4 < 5), 2 -> r0 (5 < 7), 1 -> r0 (7 == 7, lower rank)
+    assert lpt_assign([5, 1, 4, 2, 3], 2) == [[0, 1, 3], [2, 4]]
+    rng = np.random.Generator(np.random.PCG64(7))
+    for hq, hkv, world in [(32, 8, 2), (32, 8, 4), (56, 8, 8), (28, 4, 8), (28, 4, 3), (8, 2, 8)]:
+        costs = rng.uniform(1.0, 10.0, hq).tolist()
+        shards = [plan_heads_lpt(costs, hkv, world, r) for r in range(world)]
+        owned = sorted(h for s in shards for h in s.q_heads)
+        assert owned == list(range(hq))
+        qpk = hq // hkv
+        for s in shards:
+            _check_kernel_map(s, qpk)
+            if world <= hkv:  # whole kv groups
+                assert s.n_q == s.n_kv * qpk
+        loads = [sum(costs[h] for h in s.q_heads) for s in shards]
+        unit = max(costs) * (qpk if world <= hkv else 1)
+        assert max(loads) - min(loads) <= unit + 1e-9  # LPT bound: within one unit
+        assert [plan_heads_lpt(costs, hkv, world, r) for r in range(world)] == shards  # deterministic
+    # a skewed cost vector moves whole groups away from the contiguous split
+    costs = [10.0] * 8 + [1.0] * 24  # kv groups 0, 1 expensive (32/8)
+    a, b = plan_heads_lpt(costs, 8, 2, 0), plan_heads_lpt(costs, 8, 2, 1)
+    assert set(a.kv_heads) & {0, 1} and set(b.kv_heads) & {0, 1}
 
 
 def _free_port():
@@ -40,7 +77,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, result):
+def _worker(rank, world, port, result, plan):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -53,11 +90,16 @@ def _worker(rank, world, port, result):
         q = rng.standard_normal((hq, s_len, d)).astype(np.float32)
         k = rng.standard_normal((hkv, s_len, d)).astype(np.float32)
         v = rng.standard_normal((hkv, s_len, d)).astype(np.float32)
-        shards = [shard_heads(hq, hkv, world, r) for r in range(world)]
+        if plan == "lpt":
+            costs = [1.0, 5.0, 2.0, 2.0, 9.0, 1.0]  # groups of 3: {0,1,2} = 8, {3,4,5} = 12
+            shards = [plan_heads_lpt(costs, hkv, world, r) for r in range(world)]
+            assert shards[0].q_heads == (3, 4, 5)  # the dearer group goes to rank 0: gather reorders
+        else:
+            shards = [shard_heads(hq, hkv, world, r) for r in range(world)]
         me = shards[rank]
-        k_loc, v_loc = k[me.kv_begin:me.kv_end], v[me.kv_begin:me.kv_end]
+        k_loc, v_loc = k[list(me.kv_stack)], v[list(me.kv_stack)]
         outs = []
-        for h in range(me.q_begin, me.q_end):
+        for h in me.q_heads:
             tiles, cols, _ = orc.build_vs_layout_with_stats(*orc.estimate_vertical_slash(
                 q[h], k[h // (hq // hkv)], 8, 12, 16), s_len, b)
             ts, to = orc.flatten(tiles)
@@ -82,11 +124,11 @@ def _worker(rank, world, port, result):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_two_rank_gloo_sharded_layer(world):
+@pytest.mark.parametrize("world,plan", [(2, "contiguous"), (2, "lpt")])
+def test_two_rank_gloo_sharded_layer(world, plan):
     mgr = mp.Manager()
     result = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), result), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), result, plan), nprocs=world, join=True)
     assert result["shape"] == (6, 96, 16)
     assert result["max_err"] == 0.0  # same CPU computation, reassembled in head order
     assert result["t"] == float(world)  # max over ranks

@@ -189,6 +189,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="head chunks (whole kv groups) per layer in the host-buffer pipeline of the e2e leg; "
+                         "0 = auto: 1 when the job has several layers (layer l+1's copy hides behind layer l), "
+                         "one per kv group for a single layer (C2 1 chunk 1115 ms vs 4: 1138; C4 1: 187 vs 8: 165)")
     ap.add_argument("--shard", default="contiguous", choices=["contiguous", "lpt"],
                     help="q-head partition over ranks: contiguous kv-group ranges, or LPT on modeled kernel FLOPs")
     ap.add_argument("--gather", action="store_true",
@@ -400,57 +404,22 @@ def main():
 
 
 def run_e2e(args, model, torch, Q, K, V, L, stream):
-    """Public API with host buffers: per layer, H2D of Q/K/V from pinned host
-    memory (copy stream, prefetching layer l+1 during layer l), the model
-    driver's layer (driver.SparsePrefill: estimation, compaction, attention),
-    and D2H of the output into pinned host memory."""
-    dev = Q[0].device
-    slots = 2
+    """Public API with host buffers: driver.SparsePrefill.prefill_host -- per (layer, head
+    chunk) unit, H2D of Q/K/V from pinned host memory on a copy stream (unit u+1 while
+    unit u computes), the layer's estimation, compaction and attention for the chunk's
+    heads, and D2H of its output into pinned host memory on a third stream."""
+    slots = 2  # pinned host inputs for two layers, reused round-robin (host RAM)
     host_q = [Q[i % L].cpu().pin_memory() for i in range(slots)]
     host_k = [K[i % L].cpu().pin_memory() for i in range(slots)]
     host_v = [V[i % L].cpu().pin_memory() for i in range(slots)]
     host_o = [torch.empty_like(host_q[0]).pin_memory() for _ in range(slots)]
-    dq = [torch.empty_like(Q[0]) for _ in range(2)]
-    dk = [torch.empty_like(K[0]) for _ in range(2)]
-    dv = [torch.empty_like(V[0]) for _ in range(2)]
-    do = [torch.empty_like(Q[0]) for _ in range(2)]
-    h2d = torch.cuda.Stream(dev)
-    d2h = torch.cuda.Stream(dev)
+    host_layers = [(host_q[layer % slots], host_k[layer % slots], host_v[layer % slots]) for layer in range(L)]
+    host_out = [host_o[layer % slots] for layer in range(L)]
     comp = stream
+    chunks = args.e2e_chunks if args.e2e_chunks > 0 else (1 if L > 2 else K[0].shape[0])
 
     def one_step():
-        ready = [None, None]
-        done_out = [None, None]
-
-        def issue_h2d(layer):
-            slot = layer % 2
-            with torch.cuda.stream(h2d):
-                if done_out[slot] is not None:
-                    h2d.wait_event(done_out[slot])
-                dq[slot].copy_(host_q[layer % slots], non_blocking=True)
-                dk[slot].copy_(host_k[layer % slots], non_blocking=True)
-                dv[slot].copy_(host_v[layer % slots], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(h2d)
-            ready[slot] = ev
-
-        issue_h2d(0)
-        for layer in range(L):
-            slot = layer % 2
-            if layer + 1 < L:
-                issue_h2d(layer + 1)
-            comp.wait_event(ready[slot])
-            model.layer(layer, dq[slot], dk[slot], dv[slot], out=do[slot])
-            ev = torch.cuda.Event()
-            ev.record(comp)
-            with torch.cuda.stream(d2h):
-                d2h.wait_event(ev)
-                host_o[layer % slots].copy_(do[slot], non_blocking=True)
-                e2 = torch.cuda.Event()
-                e2.record(d2h)
-            done_out[slot] = e2
-        comp.wait_stream(d2h)
-        comp.wait_stream(h2d)
+        model.prefill_host(host_layers, host_out, chunks=chunks)
 
     one_step()
     torch.cuda.synchronize()
@@ -466,9 +435,10 @@ def run_e2e(args, model, torch, Q, K, V, L, stream):
     h2d_bytes = L * (Q[0].numel() + K[0].numel() + V[0].numel()) * 2
     d2h_bytes = L * Q[0].numel() * 2
     return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d_bytes),
-            "d2h_bytes_per_step": int(d2h_bytes), "steps": n,
-            "note": "public API driver.SparsePrefill.layer per layer; pinned host buffers (2-slot ring of layer "
-                    "inputs), H2D prefetch of layer l+1 overlapping layer l, D2H of every layer's output"}
+            "d2h_bytes_per_step": int(d2h_bytes), "steps": n, "head_chunks": chunks,
+            "note": "public API driver.SparsePrefill.prefill_host: pinned host buffers (inputs of two layers reused "
+                    "round-robin), per (layer, kv-group chunk) H2D on one stream overlapping the previous unit's "
+                    "estimation + attention and the D2H of the one before on another"}
 
 
 def dense_baseline(torch, q, k, v, L, ms_per_step):

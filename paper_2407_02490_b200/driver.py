@@ -91,12 +91,14 @@ class PatternTable:
                 return cfg.block_size
         return default
 
-    def device_groups(self, layer: int, device) -> list:
-        """[(config, int32 q-head ids on ``device``, count)] in first-appearance order."""
-        key = (layer, str(torch.device(device)))
+    def device_groups(self, layer: int, device, heads: tuple | None = None) -> list:
+        """[(config, int32 q-head ids on ``device``, count)] in first-appearance order;
+        ``heads`` = (h0, h1) restricts to that head range (ids then relative to h0)."""
+        h0, h1 = heads if heads is not None else (0, self.n_heads)
+        key = (layer, str(torch.device(device)), h0, h1)
         if key not in self._groups:
             groups: "OrderedDict[HeadPatternConfig, list[int]]" = OrderedDict()
-            for h, cfg in enumerate(self.layers[layer]):
+            for h, cfg in enumerate(self.layers[layer][h0:h1]):
                 groups.setdefault(cfg, []).append(h)
             self._groups[key] = [(cfg, torch.tensor(ids, dtype=torch.int32, device=device), len(ids))
                                  for cfg, ids in groups.items()]
@@ -131,6 +133,87 @@ class SparsePrefill:
         sc = self.scale if self.scale is not None else 1.0 / math.sqrt(q.shape[-1])
         return sparse_prefill_attention(q, k, v, cfgs, self.table.block_size(layer, self.default_block), sc, out,
                                         stream, return_layout, groups=self.table.device_groups(layer, q.device))
+
+    def layer_heads(self, layer: int, h0: int, h1: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out=None,
+                    stream=None):
+        """The layer restricted to q-heads [h0, h1) (whole kv groups): q [h1-h0, S, d] and
+        the k/v heads they read."""
+        if q.shape[0] != h1 - h0:
+            raise ValueError(f"layer {layer}: q has {q.shape[0]} heads for the head range [{h0}, {h1})")
+        cfgs = self.table.layer(layer)[h0:h1]
+        sc = self.scale if self.scale is not None else 1.0 / math.sqrt(q.shape[-1])
+        return sparse_prefill_attention(q, k, v, cfgs, self.table.block_size(layer, self.default_block), sc, out,
+                                        stream, groups=self.table.device_groups(layer, q.device, (h0, h1)))
+
+    def prefill_host(self, host_layers, host_out, chunks: int = 1, device=None):
+        """Host-resident model pass: ``host_layers`` = [(q, k, v)] per layer (pinned CPU
+        tensors [Hq, S, d] / [Hkv, S, d]), outputs into ``host_out`` (pinned CPU [Hq, S, d]
+        per layer).  Each layer is split into ``chunks`` head ranges of whole kv groups;
+        unit u = (layer, chunk) is copied in on one stream while unit u-1 computes and
+        unit u-2 is copied out on a third, through two device slots, so the PCIe
+        transfers in both directions overlap the kernels (the first and last units'
+        copies are the only exposed ones: finer chunks shrink them).  Returns after
+        enqueueing; the caller synchronises."""
+        if len(host_layers) > self.table.n_layers or len(host_out) != len(host_layers):
+            raise ValueError("one output per layer, at most the table's layers")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        q0, k0, _ = host_layers[0]
+        hq, hkv = q0.shape[0], k0.shape[0]
+        if hq != self.table.n_heads or hq % hkv:
+            raise ValueError("head counts do not match the pattern table")
+        qpk = hq // hkv
+        chunks = max(1, min(int(chunks), hkv))
+        bounds = [(hkv * c // chunks, hkv * (c + 1) // chunks) for c in range(chunks)]
+        units = [(layer, g0, g1) for layer in range(len(host_layers)) for g0, g1 in bounds]
+        gmax = max(g1 - g0 for g0, g1 in bounds)
+        S, d = q0.shape[1], q0.shape[2]
+        slots = [dict(q=torch.empty((gmax * qpk, S, d), dtype=q0.dtype, device=dev),
+                      k=torch.empty((gmax, S, d), dtype=q0.dtype, device=dev),
+                      v=torch.empty((gmax, S, d), dtype=q0.dtype, device=dev),
+                      o=torch.empty((gmax * qpk, S, d), dtype=q0.dtype, device=dev)) for _ in range(2)]
+        comp = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_copy_streams") or self._copy_streams[0].device != dev:
+            self._copy_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        h2d, d2h = self._copy_streams
+        ready, freed = [None, None], [None, None]
+
+        def issue_in(u):
+            layer, g0, g1 = units[u]
+            s = slots[u % 2]
+            qh, kh, vh = host_layers[layer]
+            with torch.cuda.stream(h2d):
+                if freed[u % 2] is not None:
+                    h2d.wait_event(freed[u % 2])  # compute of unit u-2 has read the slot
+                s["q"][: (g1 - g0) * qpk].copy_(qh[g0 * qpk:g1 * qpk], non_blocking=True)
+                s["k"][: g1 - g0].copy_(kh[g0:g1], non_blocking=True)
+                s["v"][: g1 - g0].copy_(vh[g0:g1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+            ready[u % 2] = ev
+
+        out_done = [None, None]
+        issue_in(0)
+        for u, (layer, g0, g1) in enumerate(units):
+            if u + 1 < len(units):
+                issue_in(u + 1)
+            s = slots[u % 2]
+            n_q = (g1 - g0) * qpk
+            comp.wait_event(ready[u % 2])
+            if out_done[u % 2] is not None:
+                comp.wait_event(out_done[u % 2])  # the slot's previous output has been copied out
+            self.layer_heads(layer, g0 * qpk, g1 * qpk, s["q"][:n_q], s["k"][: g1 - g0], s["v"][: g1 - g0],
+                             out=s["o"][:n_q])
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            freed[u % 2] = ev
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev)
+                host_out[layer][g0 * qpk:g1 * qpk].copy_(s["o"][:n_q], non_blocking=True)
+                e2 = torch.cuda.Event()
+                e2.record(d2h)
+            out_done[u % 2] = e2
+        comp.wait_stream(d2h)
+        comp.wait_stream(h2d)
 
     def __call__(self, layers_qkv, stream=None):
         """``layers_qkv``: iterable of (q, k, v) per layer, in layer order; yields outputs."""

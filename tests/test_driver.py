@@ -72,3 +72,30 @@ def test_driver_matches_layer_pipeline(P):
         assert torch.equal(outs[l], want)
     with pytest.raises(ValueError):
         SparsePrefill(table).layer(0, layers[0][0][:4].contiguous(), layers[0][1], layers[0][2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunks", [1, 2])
+def test_prefill_host_pipeline_matches_device_layers(P, chunks):
+    """SparsePrefill.prefill_host (pinned host in/out, per kv-group chunk H2D / compute / D2H
+    on three streams through two device slots) returns exactly the device-side layers."""
+    import torch
+
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    hq, hkv, s, d = 8, 2, 2048, 128
+    table = PatternTable([[P.VerticalSlash(64, 256)] * 3 + [P.BlockSparse(8)] + [P.AShape(64, 512)] * 4,
+                          [P.BlockSparse(4)] * 8,
+                          [P.VerticalSlash(100, 300)] * 8])
+    layers = [tuple(torch.randn(h, s, d, generator=g, device=dev).to(torch.bfloat16) for h in (hq, hkv, hkv))
+              for _ in range(3)]
+    model = SparsePrefill(table)
+    want = [model.layer(i, *layers[i]).cpu() for i in range(3)]
+    host_layers = [tuple(t.cpu().pin_memory() for t in qkv) for qkv in layers]
+    host_out = [torch.zeros((hq, s, d), dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    model.prefill_host(host_layers, host_out, chunks=chunks)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert torch.equal(host_out[i], want[i]), i

@@ -74,6 +74,9 @@ constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
+#ifndef SPF_MIN_SMEM
+#define SPF_MIN_SMEM 0
+#endif
 #ifndef SPF_KV_MAJOR
 #define SPF_KV_MAJOR 0  // kv-head-major item order: 0.7-1.1 % slower on C2-shaped VS / A-shape layers
 #endif
@@ -908,9 +911,12 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
     tv2 = tv;
   }
   auto kern = sparse_attn_fwd_kernel<kD, kSplit>;
+  // SPF_MIN_SMEM (experiment knob, default 0): launch with at least this much dynamic shared
+  // memory, e.g. 120000 to hold the kernel to one CTA per SM
+  constexpr int kLaunchSmem = L::kSmem > SPF_MIN_SMEM ? L::kSmem : SPF_MIN_SMEM;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaunchSmem);
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(attn smem)");
     attr_done = true;
   }
@@ -920,7 +926,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
   if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
   const float scale_log2 = a.scale * 1.4426950408889634f;
   note_launches(1);
-  kern<<<(unsigned)grid, kThreadsT<kSplit>, L::kSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
+  kern<<<(unsigned)grid, kThreadsT<kSplit>, kLaunchSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
   return check_cuda(cudaGetLastError(), "sparse_attn_fwd launch");
 }
 

@@ -22,10 +22,11 @@ cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * hq, "bs": [P.BlockSparse(100)] * h
         "tiny": [P.AShape(1, 64)] * hq, "small": [P.AShape(64, 640)] * hq}[cfg]
 pair = torch.arange(hq, dtype=torch.int32, device="cuda")  # AB_PAIR=1: every head through the paired-box kernel
 n_pair = hq if os.environ.get("AB_PAIR", "0") == "1" else 0
+n_pairs = [hq if os.environ.get(f"AB_PAIR_{x}", os.environ.get("AB_PAIR", "0")) == "1" else 0 for x in "AB"]
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p
-def run(lib):
+def run(lib, n_pair):
     lib.spf_sparse_flash_rows_ex.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp,
                                              ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp]
@@ -39,7 +40,7 @@ ts = [[], []]
 for r in range(int(os.environ.get("AB_REPS", "12"))):
     for i, lib in enumerate(libs):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(); run(lib); e1.record(); torch.cuda.synchronize()
+        e0.record(); run(lib, n_pairs[i]); e1.record(); torch.cuda.synchronize()
         if r >= 2:
             ts[i].append(e0.elapsed_time(e1))
 print(cfg, "A %.3f ms  B %.3f ms  (B/A %.3f)" % (statistics.median(ts[0]), statistics.median(ts[1]),

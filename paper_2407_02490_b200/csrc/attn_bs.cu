@@ -38,8 +38,17 @@ constexpr int kThreads = 192;
 struct PairDesc {
   int box[2];    // first key of each box (-1: absent)
   int width[2];  // keys of the box inside the sequence
+  int seg[2];    // union pairing: bit h set = row block h of the CTA owns the box (0: absent)
   int end;       // 1: no more steps
 };
+
+// SPF_PAIR_UNION=1 (experiment): a step takes the next TWO items of the union of the
+// CTA's two tile lists (descending), so every row exponentiates up to 128 keys per step --
+// the union kernel's work in half the steps, for heads without residual columns.
+#ifndef SPF_PAIR_UNION
+#define SPF_PAIR_UNION 0
+#endif
+constexpr bool kUnion = SPF_PAIR_UNION != 0;
 
 // !kDB (the default): two CTAs per SM, one S with P written over it -- a serial
 // softmax -> PV -> QK chain per CTA that the co-resident CTA interleaves with.
@@ -51,6 +60,7 @@ struct PairDesc {
 #define SPF_PAIR_DB 0
 #endif
 constexpr bool kDB = SPF_PAIR_DB != 0;
+static_assert(!(kUnion && kDB), "union pairing is written for the single-buffered chain");
 constexpr int kStages = kDB ? 2 : 1;
 
 struct PCtrl {
@@ -146,18 +156,51 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
 #pragma unroll
       for (int a = 0; a < L::kAtoms; ++a)
         tma_load_3d(smem + L::kOffQ + a * (kRows * 128), &tm_q, &ctrl->q_full, a * 64, R0, h);
-      for (int64_t i = 0; i <= steps; ++i) {
+      int64_t j0 = n0 - 1, j1 = n1 - 1;  // union walk: next candidate of each ascending list
+      auto next_item = [&](int& start, int& seg) {
+        const bool h0 = j0 >= 0, h1 = j1 >= 0;
+        if (!h0 && !h1) return false;
+        const int s0 = h0 ? p.tile_starts[a0 + j0] : 0;
+        const int s1 = h1 ? p.tile_starts[a1 + j1] : 0;
+        if (h0 && (!h1 || s0 >= s1)) {
+          start = s0;
+          seg = 1;
+          --j0;
+          if (h1 && s1 == s0) {
+            seg = 3;
+            --j1;
+          }
+        } else {
+          start = s1;
+          seg = 2;
+          --j1;
+        }
+        return true;
+      };
+      for (int64_t i = 0; kUnion || i <= steps; ++i) {
         const int sd = (int)(i & 1);
         mbar_wait(&ctrl->d_empty[sd], (int)((i >> 1) & 1) ^ 1);
         PairDesc& d = ctrl->desc[sd];
-        if (i == steps) {
+        int box[2], seg[2];
+        bool more = true;
+        if (kUnion) {
+          more = next_item(box[0], seg[0]);
+          if (more && !next_item(box[1], seg[1])) {
+            box[1] = S;
+            seg[1] = 0;
+          }
+        } else {
+          more = i < steps;
+          box[0] = i < n0 ? p.tile_starts[a0 + n0 - 1 - i] : -1;  // descending: the diagonal block first
+          box[1] = i < n1 ? p.tile_starts[a1 + n1 - 1 - i] : -1;
+          seg[0] = box[0] >= 0 ? 1 : 0;
+          seg[1] = box[1] >= 0 ? 2 : 0;
+        }
+        if (!more) {
           d.end = 1;
           mbar_arrive(&ctrl->d_full[sd]);
           break;
         }
-        int box[2];
-        box[0] = i < n0 ? p.tile_starts[a0 + n0 - 1 - i] : -1;  // descending: the diagonal block first
-        box[1] = i < n1 ? p.tile_starts[a1 + n1 - 1 - i] : -1;
         // K(i): its stage is free once QK(i - kStages) retired
         const int st = (int)(i % kStages);
         const int sph = (int)((i / kStages) & 1);
@@ -165,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
         mbar_arrive_expect_tx(&ctrl->k_full[st], 2 * L::kTxBox);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-          const int row = box[b] >= 0 ? box[b] : S;  // absent: past the end -> zero fill
+          const int row = seg[b] ? box[b] : S;  // absent: past the end -> zero fill
 #pragma unroll
           for (int a = 0; a < L::kAtoms; ++a)
             tma_load_3d(smem + L::kOffK + st * L::kStage + a * L::kAtomStage + b * (kBox * 128), &tm_k,
@@ -174,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           d.box[b] = box[b];
-          d.width[b] = box[b] >= 0 ? min(kBox, S - box[b]) : 0;
+          d.width[b] = seg[b] ? min(kBox, S - box[b]) : 0;
+          d.seg[b] = seg[b];
         }
         d.end = 0;
         mbar_arrive(&ctrl->d_full[sd]);
@@ -183,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
         mbar_arrive_expect_tx(&ctrl->v_full[st], 2 * L::kTxBox);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-          const int row = box[b] >= 0 ? box[b] : S;
+          const int row = seg[b] ? box[b] : S;
 #pragma unroll
           for (int a = 0; a < L::kAtoms; ++a)
             tma_load_3d(smem + L::kOffV + st * L::kStage + a * L::kAtomStage + b * (kBox * 128), &tm_v,
@@ -258,6 +302,104 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
       mbar_wait(&ctrl->d_full[sd], (t >> 1) & 1);
       const PairDesc& d = ctrl->desc[sd];
       if (d.end) break;
+      if (kUnion) {
+        // both boxes may belong to this row's block: up to 128 keys per row
+        int lo[2], hi[2];
+        bool any = false;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          lo[b] = 0;
+          hi[b] = 0;
+          if (((d.seg[b] >> half) & 1) && q < S) {
+            const int bx = d.box[b];
+            lo[b] = max(0, -bx);
+            hi[b] = min(d.width[b], q - bx + 1);
+          }
+          any = any || hi[b] > lo[b];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
+        const bool warp_skip = !__any_sync(0xffffffffu, any);
+        mbar_wait(&ctrl->s_full[t & 1], (t >> 1) & 1);
+        tc_fence_after();
+        uint32_t x[kKeys];
+        float alpha = 1.f;
+        bool rescale = false;
+        if (!warp_skip) {
+          tmem_ld32x32b_x64(tmem + lane_off + s_col(t), x);
+          tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + kBox, x + kBox);
+          tmem_wait_ld();
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            if (!(lo[b] == 0 && hi[b] == kBox)) {
+#pragma unroll
+              for (int j = 0; j < kBox; ++j)
+                x[b * kBox + j] = (j >= lo[b] && j < hi[b]) ? x[b * kBox + j] : 0xff800000u;
+            }
+          }
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < kKeys; j += 8) {
+            mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
+            mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
+            mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
+            mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
+          }
+          const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+          if (any) {
+            const float m_tile = mx * scale_log2;
+            if (m_run == -INFINITY) {
+              m_run = m_tile;
+            } else if (m_tile > m_run + 8.f) {
+              alpha = exp2f(m_run - m_tile);
+              m_run = m_tile;
+              rescale = true;
+            }
+          }
+          const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+          const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
+          const uint64_t m2 = pack_f32x2(neg_m, neg_m);
+          uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+          for (int j = 0; j < kKeys; j += 2) {
+            const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
+            float y0, y1;
+            unpack_f32x2(yv, y0, y1);
+            const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+            const uint64_t pp = pack_f32x2(p0, p1);
+            switch ((j >> 1) & 3) {
+              case 0: s0 = fadd2(s0, pp); break;
+              case 1: s1 = fadd2(s1, pp); break;
+              case 2: s2 = fadd2(s2, pp); break;
+              default: s3 = fadd2(s3, pp); break;
+            }
+            x[j >> 1] = pack_bf16x2(p0, p1);  // in place: x[j/2] is already consumed
+          }
+          float sa, sb;
+          unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb);
+          l_run = l_run * alpha + (sa + sb);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kKeys / 2; ++j) x[j] = 0u;
+        }
+        if (t > 0 && __any_sync(0xffffffffu, rescale)) {  // S(t) ready implies PV(t-1) retired
+#pragma unroll
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t o[32];
+            tmem_ld32x32b_x32((tmem + lane_off + L::kColO) + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
+            tmem_st32x32b_x32((tmem + lane_off + L::kColO) + c, o);
+          }
+        }
+        tmem_st32x32b_x32(tmem + lane_off + p_col(t), x);
+        tmem_st32x32b_x32(tmem + lane_off + p_col(t) + 32, x + 32);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&ctrl->p_full[t & 1]);
+        continue;
+      }
       const int box = d.box[half];
       int hi = 0;
       if (box >= 0 && q < S) hi = min(d.width[half], q - box + 1);  // causal inside the block

@@ -34,7 +34,10 @@ struct BlockTopK {
   using Key = typename std::conditional<sizeof(T) == 8, uint64_t, uint32_t>::type;
   // 8-bit digits: a 256-bin histogram is zeroed and scanned with one bin per thread (rows
   // of a few thousand candidates pay more for 2048-bin rounds than for one extra round)
-  static constexpr int kBits = 8;
+#ifndef SPF_TOPK_BITS32
+#define SPF_TOPK_BITS32 8
+#endif
+  static constexpr int kBits = sizeof(T) == 4 ? SPF_TOPK_BITS32 : 8;
   static constexpr int kBins = 1 << kBits;
   static constexpr int kKeyBits = sizeof(Key) * 8;
   using Scan = cub::BlockScan<int, kThreads>;

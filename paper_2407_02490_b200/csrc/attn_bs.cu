@@ -60,7 +60,6 @@ constexpr bool kUnion = SPF_PAIR_UNION != 0;
 #define SPF_PAIR_DB 0
 #endif
 constexpr bool kDB = SPF_PAIR_DB != 0;
-static_assert(!(kUnion && kDB), "union pairing is written for the single-buffered chain");
 constexpr int kStages = kDB ? 2 : 1;
 
 struct PCtrl {
@@ -382,7 +381,17 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
 #pragma unroll
           for (int j = 0; j < kKeys / 2; ++j) x[j] = 0u;
         }
-        if (t > 0 && __any_sync(0xffffffffu, rescale)) {  // S(t) ready implies PV(t-1) retired
+        if (kDB) {  // S(t) consumed (QK(t+2) may overwrite it)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctrl->s_free[t & 1]);
+        }
+        if (t > 0 && __any_sync(0xffffffffu, rescale)) {
+          // single S: S(t) ready implies PV(t-1) retired; double-buffered: wait for PV(t-1)
+          if (kDB) {
+            mbar_wait(&ctrl->v_empty[(t - 1) % kStages], ((t - 1) / kStages) & 1);
+            tc_fence_after();
+          }
 #pragma unroll
           for (int c = 0; c < kD; c += 32) {
             uint32_t o[32];

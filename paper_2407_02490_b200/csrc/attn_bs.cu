@@ -33,7 +33,13 @@ namespace {
 constexpr int kRows = 128;
 constexpr int kBox = 64;
 constexpr int kKeys = 128;  // two boxes per step
-constexpr int kThreads = 192;
+// SPF_PAIR_HALVES=2 (with union pairing): two softmax warps per TMEM lane quarter, each
+// exponentiating 64 of a row's 128 keys (both read all 128 for the max)
+#ifndef SPF_PAIR_HALVES
+#define SPF_PAIR_HALVES 1
+#endif
+constexpr int kHalves = SPF_PAIR_HALVES;
+constexpr int kThreads = 64 + 128 * kHalves;
 
 struct PairDesc {
   int box[2];    // first key of each box (-1: absent)
@@ -50,6 +56,7 @@ struct PairDesc {
 #endif
 constexpr bool kUnion = SPF_PAIR_UNION != 0;
 
+
 // !kDB (the default): two CTAs per SM, one S with P written over it -- a serial
 // softmax -> PV -> QK chain per CTA that the co-resident CTA interleaves with.
 // kDB (SPF_PAIR_DB=1): one CTA per SM owning all 512 TMEM columns -- S(t) in
@@ -60,6 +67,7 @@ constexpr bool kUnion = SPF_PAIR_UNION != 0;
 #define SPF_PAIR_DB 0
 #endif
 constexpr bool kDB = SPF_PAIR_DB != 0;
+static_assert(kHalves == 1 || (kHalves == 2 && kUnion && kDB), "split softmax rows: union pairing, one CTA per SM");
 constexpr int kStages = kDB ? 2 : 1;
 
 struct PCtrl {
@@ -69,6 +77,7 @@ struct PCtrl {
   uint64_t s_full[2], s_free[2], p_full[2], o_ready;
   uint32_t tmem_base, pad;
   PairDesc desc[2];
+  float lsum[2][128];  // split softmax: each half's row sums, combined in the epilogue
 };
 
 template <int kD>
@@ -126,10 +135,10 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
       mbar_init(&ctrl->v_full[s], 1);
       mbar_init(&ctrl->v_empty[s], 1);
       mbar_init(&ctrl->d_full[s], 1);
-      mbar_init(&ctrl->d_empty[s], 4);
+      mbar_init(&ctrl->d_empty[s], 4 * kHalves);
       mbar_init(&ctrl->s_full[s], 1);
-      mbar_init(&ctrl->s_free[s], 4);
-      mbar_init(&ctrl->p_full[s], 128);
+      mbar_init(&ctrl->s_free[s], 4 * kHalves);
+      mbar_init(&ctrl->p_full[s], 128 * kHalves);
     }
     mbar_init(&ctrl->o_ready, 1);
     fence_mbar_init();
@@ -291,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
     // rows 64..127 (quarters 2, 3) = row block r1 -> S columns 64..127 (box 1)
     const int quarter = warp & 3;
     const int half = quarter >> 1;
+    const int kh = kHalves > 1 ? (warp - 2) >> 2 : 0;  // key half of a 128-key step (split softmax)
     const int row = quarter * 32 + lane;
     const int q = R0 + row;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -321,20 +331,22 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
         const bool warp_skip = !__any_sync(0xffffffffu, any);
         mbar_wait(&ctrl->s_full[t & 1], (t >> 1) & 1);
         tc_fence_after();
-        uint32_t x[kKeys];
+        uint32_t x[kKeys];  // x[0, 64): this warp's own key half (box kh), x[64, 128): the other box
         float alpha = 1.f;
         bool rescale = false;
         if (!warp_skip) {
-          tmem_ld32x32b_x64(tmem + lane_off + s_col(t), x);
-          tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + kBox, x + kBox);
+          tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + kh * kBox, x);
+          tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + (kh ^ 1) * kBox, x + kBox);
           tmem_wait_ld();
+          const int lo_a = kh ? lo[1] : lo[0], hi_a = kh ? hi[1] : hi[0];
+          const int lo_b = kh ? lo[0] : lo[1], hi_b = kh ? hi[0] : hi[1];
+          if (!(lo_a == 0 && hi_a == kBox)) {
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            if (!(lo[b] == 0 && hi[b] == kBox)) {
+            for (int j = 0; j < kBox; ++j) x[j] = (j >= lo_a && j < hi_a) ? x[j] : 0xff800000u;
+          }
+          if (!(lo_b == 0 && hi_b == kBox)) {
 #pragma unroll
-              for (int j = 0; j < kBox; ++j)
-                x[b * kBox + j] = (j >= lo[b] && j < hi[b]) ? x[b * kBox + j] : 0xff800000u;
-            }
+            for (int j = 0; j < kBox; ++j) x[kBox + j] = (j >= lo_b && j < hi_b) ? x[kBox + j] : 0xff800000u;
           }
           float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
@@ -359,8 +371,10 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
           const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
           const uint64_t m2 = pack_f32x2(neg_m, neg_m);
           uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+          // own keys first (x[0, 64)), then -- one warp per quarter -- the other box (x[64, 128));
+          // p packs in place: x[j/2] is already consumed
 #pragma unroll
-          for (int j = 0; j < kKeys; j += 2) {
+          for (int j = 0; j < kKeys / kHalves; j += 2) {
             const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
             float y0, y1;
             unpack_f32x2(yv, y0, y1);
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
               case 2: s2 = fadd2(s2, pp); break;
               default: s3 = fadd2(s3, pp); break;
             }
-            x[j >> 1] = pack_bf16x2(p0, p1);  // in place: x[j/2] is already consumed
+            x[j >> 1] = pack_bf16x2(p0, p1);
           }
           float sa, sb;
           unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb);
@@ -393,17 +407,22 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
             tc_fence_after();
           }
 #pragma unroll
-          for (int c = 0; c < kD; c += 32) {
+          for (int c = 0; c < kD / kHalves; c += 32) {  // this half's O columns
             uint32_t o[32];
-            tmem_ld32x32b_x32((tmem + lane_off + L::kColO) + c, o);
+            const uint32_t oc = L::kColO + kh * (kD / kHalves) + c;
+            tmem_ld32x32b_x32(tmem + lane_off + oc, o);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-            tmem_st32x32b_x32((tmem + lane_off + L::kColO) + c, o);
+            tmem_st32x32b_x32(tmem + lane_off + oc, o);
           }
         }
-        tmem_st32x32b_x32(tmem + lane_off + p_col(t), x);
-        tmem_st32x32b_x32(tmem + lane_off + p_col(t) + 32, x + 32);
+        if (kHalves == 1) {
+          tmem_st32x32b_x32(tmem + lane_off + p_col(t), x);
+          tmem_st32x32b_x32(tmem + lane_off + p_col(t) + 32, x + 32);
+        } else {
+          tmem_st32x32b_x32(tmem + lane_off + p_col(t) + kh * 32, x);  // P of this half's 64 keys
+        }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&ctrl->p_full[t & 1]);
@@ -510,13 +529,18 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
     // ---- epilogue: O / l -> global (bf16) ----
     mbar_wait(&ctrl->o_ready, 0);
     tc_fence_after();
+    if (kHalves > 1) {  // the halves' row sums
+      ctrl->lsum[kh][row] = l_run;
+      named_bar_sync(1, 128 * kHalves);
+      l_run = ctrl->lsum[0][row] + ctrl->lsum[1][row];
+    }
     const float inv = (t > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
     const int dout = p.d_out;
     const int64_t obase = ((int64_t)h * S + min(q, S - 1)) * dout;
-    if (p.lse != nullptr && q < S)
+    if (p.lse != nullptr && q < S && kh == 0)
       p.lse[(int64_t)h * S + q] = (t > 0 && l_run > 0.f) ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
 #pragma unroll
-    for (int c = 0; c < kD; c += 32) {
+    for (int c = kh * (kD / kHalves); c < (kh + 1) * (kD / kHalves); c += 32) {
       uint32_t o[32];
       __syncwarp();
       tmem_ld32x32b_x32((tmem + lane_off + L::kColO) + c, o);

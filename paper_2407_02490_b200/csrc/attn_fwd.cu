@@ -74,6 +74,9 @@ constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
+#ifndef SPF_DESC_UNDER_LD
+#define SPF_DESC_UNDER_LD 1  // row ranges from the step descriptor computed under the S load (0.1-0.2 %)
+#endif
 #ifndef SPF_MIN_SMEM
 #define SPF_MIN_SMEM 0
 #endif
@@ -662,6 +665,25 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         tmem_ld32x32b_x32(tmem + lane_off + s_col + c0, x);
         tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
       }
+#if SPF_DESC_UNDER_LD
+      // valid key slots for this row, [lo, hi), computed while the TMEM load is in flight
+      int lo = 0, hi = 0;
+      if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
+        if (kind == kTile) {
+          lo = max(0, -d.box);
+          hi = min(d.width, min(S - d.box, q - d.box + 1));
+        } else {
+          int a = 0, b = d.width;
+          while (a < b) {
+            const int m = (a + b) >> 1;
+            if (d.pmax[m] <= q) a = m + 1; else b = m;
+          }
+          hi = a;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+#endif
       tmem_wait_ld();
       if (tr0 && SPF_TRACE == 3) trace1(1, t, 0);
       if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
@@ -669,7 +691,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctrl->s_free[0]);
       }
-
+#if !SPF_DESC_UNDER_LD
       // valid key slots for this row: a contiguous range [lo, hi)
       int lo = 0, hi = 0;
       if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
@@ -687,6 +709,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+#endif
       if (!__any_sync(0xffffffffu, hi > lo)) {
         // none of this warp's rows sees the step (the other row block's tile of a union
         // step, a block-sparse block of the other row): P = 0, softmax state unchanged

@@ -74,6 +74,9 @@ constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
+#ifndef SPF_P_EARLY
+#define SPF_P_EARLY 0  // 1: P(t) stored to TMEM before the row sum / O rescale
+#endif
 #ifndef SPF_DESC_UNDER_LD
 #define SPF_DESC_UNDER_LD 1  // row ranges from the step descriptor computed under the S load (0.1-0.2 %)
 #endif
@@ -801,6 +804,18 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         }
       }
       if (tr0 && SPF_TRACE == 3) trace1(1, t, 2);  // after the exponentials
+#if SPF_P_EARLY
+      // P(t) -> TMEM right away (its buffer was last read by PV(t-2), retired once S(t) was
+      // ready); the row sum and an O rescale proceed while the store drains
+      if (kSepP<kSplit>) {
+        const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
+        if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);
+        else tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
+      } else {
+        tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
+        if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      }
+#endif
       float sa, sb2;
       unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
       const float sum = sa + sb2;
@@ -825,6 +840,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           tmem_st32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
         }
       }
+#if !SPF_P_EARLY
       // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
       if (kSepP<kSplit>) {
         const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
@@ -834,6 +850,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
         if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
       }
+#endif
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full[sb]);

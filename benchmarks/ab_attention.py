@@ -19,10 +19,13 @@ gen = g_iid_qkv if os.environ.get("AB_GEN", "local") == "iid" else g_local_qkv
 q, k, v = gen(hq, 8, seq, 128, seed=0, device="cuda")
 cfg = os.environ.get("AB_CFG", "vs")
 cfgs = {"vs": [P.VerticalSlash(1000, 6096)] * hq, "bs": [P.BlockSparse(100)] * hq, "as": [P.AShape(128, 4096)] * hq,
-        "tiny": [P.AShape(1, 64)] * hq, "small": [P.AShape(64, 640)] * hq}[cfg]
-pair = torch.arange(hq, dtype=torch.int32, device="cuda")  # AB_PAIR=1: every head through the paired-box kernel
-n_pair = hq if os.environ.get("AB_PAIR", "0") == "1" else 0
-n_pairs = [hq if os.environ.get(f"AB_PAIR_{x}", os.environ.get("AB_PAIR", "0")) == "1" else 0 for x in "AB"]
+        "tiny": [P.AShape(1, 64)] * hq, "small": [P.AShape(64, 640)] * hq,
+        # C2's mixed Block-Sparse layers: BS(100) on heads 7 and 23, VS elsewhere
+        "mix": [P.BlockSparse(100) if h % 16 == 7 else P.VerticalSlash(1000, 6096) for h in range(hq)]}[cfg]
+# AB_PAIR=1: every head through the paired-box kernel; AB_CFG=mix lists its Block-Sparse heads
+pair_ids = [h for h in range(hq) if h % 16 == 7] if cfg == "mix" else list(range(hq))
+pair = torch.tensor(pair_ids, dtype=torch.int32, device="cuda")
+n_pairs = [len(pair_ids) if os.environ.get(f"AB_PAIR_{x}", os.environ.get("AB_PAIR", "0")) == "1" else 0 for x in "AB"]
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p

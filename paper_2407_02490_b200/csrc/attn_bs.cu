@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
   const int item = blockIdx.x;
   const int h = p.pair_heads[item / n_ctile];
   if (h < 0 || h >= p.Hq) return;
+  if (!pair_preferred(p.pair_stats, item / n_ctile)) return;  // the union kernel runs this head
   const int ct = n_ctile - 1 - item % n_ctile;
   const int kvh = h / (p.Hq / p.Hkv);
   const int S = p.S;
@@ -571,6 +572,42 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
   }
 }
 
+// Per listed head: sum over the 128-row CTAs of |tiles(r0) U tiles(r1)| (union kernel steps) and
+// max(n0, n1) (paired-box steps).  Grid (n_pair, kStatCtas), one warp per row-block pair; the
+// shared tiles are counted by binary-searching r0's starts in r1's ascending list.
+constexpr int kStatCtas = 32;
+__global__ void __launch_bounds__(256) pair_stats_kernel(const AttnArgs p, int n_rows,
+                                                          unsigned long long* __restrict__ stats) {
+  const int h = p.pair_heads[blockIdx.x];
+  if (h < 0 || h >= p.Hq) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_pairs = (n_rows + 1) / 2;
+  unsigned long long u_sum = 0, m_sum = 0;
+  for (int pp = blockIdx.y * 8 + warp; pp < n_pairs; pp += gridDim.y * 8) {
+    const int64_t row = (int64_t)h * n_rows + 2 * pp;
+    const int64_t a0 = p.tile_offsets[row], n0 = p.tile_offsets[row + 1] - a0;
+    const bool has1 = 2 * pp + 1 < n_rows;
+    const int64_t a1 = has1 ? p.tile_offsets[row + 1] : 0, n1 = has1 ? p.tile_offsets[row + 2] - a1 : 0;
+    int common = 0;
+    for (int64_t i = lane; i < n0; i += 32) {
+      const int x = p.tile_starts[a0 + i];
+      int64_t lo = 0, hi = n1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (p.tile_starts[a1 + mid] < x) lo = mid + 1; else hi = mid;
+      }
+      common += (lo < n1 && p.tile_starts[a1 + lo] == x) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) common += __shfl_xor_sync(0xffffffffu, common, o);
+    u_sum += (unsigned long long)(n0 + n1 - common);
+    m_sum += (unsigned long long)(n0 > n1 ? n0 : n1);
+  }
+  if (lane == 0 && (u_sum | m_sum)) {
+    atomicAdd(&stats[2 * blockIdx.x], u_sum);
+    atomicAdd(&stats[2 * blockIdx.x + 1], m_sum);
+  }
+}
+
 template <int kD>
 int launch_pair_impl(const AttnArgs& a, cudaStream_t stream) {
   using L = PLayout<kD>;
@@ -599,6 +636,15 @@ int launch_pair_impl(const AttnArgs& a, cudaStream_t stream) {
 
 bool attn_pair_supported(const AttnArgs& a) {
   return !a.split && !a.out_f32 && a.B == kBox && (a.kD == 128 || a.kD == 64) && a.work_order == nullptr;
+}
+
+int launch_pair_stats(const AttnArgs& a, unsigned long long* stats, cudaStream_t stream) {
+  int rc = check_cuda(cudaMemsetAsync(stats, 0, sizeof(unsigned long long) * 2 * a.n_pair, stream), "pair stats memset");
+  if (rc) return rc;
+  const int n_rows = (a.S + kBox - 1) / kBox;
+  note_launches(1);
+  pair_stats_kernel<<<dim3((unsigned)a.n_pair, kStatCtas), 256, 0, stream>>>(a, n_rows, stats);
+  return check_cuda(cudaGetLastError(), "pair stats launch");
 }
 
 int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream) {

@@ -216,7 +216,10 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   const int kvh = h / (p.Hq / p.Hkv);
 #endif
   for (int i = 0; i < p.n_pair; ++i)
-    if (p.pair_heads[i] == h) return;  // run by the paired-box kernel (attn_bs.cu)
+    if (p.pair_heads[i] == h) {
+      if (pair_preferred(p.pair_stats, i)) return;  // run by the paired-box kernel (attn_bs.cu)
+      break;
+    }
   const int S = p.S, B = p.B;
   const int n_rows = (S + B - 1) / B;
   const int R0 = ct * kRows;

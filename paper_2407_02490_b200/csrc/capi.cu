@@ -133,6 +133,30 @@ int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const voi
                                   workspace, workspace_bytes, stream);
 }
 
+}  // extern "C"
+
+namespace {
+// Per-device scratch for the routing statistics (grown on demand; cudaMalloc synchronises,
+// so it happens once per device in practice).
+unsigned long long* pair_stats_scratch(int n_pair) {
+  constexpr int kMaxDev = 64;
+  static unsigned long long* buf[kMaxDev] = {};
+  static int cap[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  if (cap[dev] < n_pair) {
+    if (buf[dev] != nullptr) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    const int want = n_pair < 256 ? 256 : n_pair;
+    if (cudaMalloc(&buf[dev], sizeof(unsigned long long) * 2 * want) != cudaSuccess) return nullptr;
+    cap[dev] = want;
+  }
+  return buf[dev];
+}
+}  // namespace
+
+extern "C" {
+
 int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,
@@ -217,7 +241,14 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
     a.pair_heads = pair_heads;
     a.n_pair = n_pair_heads;
     if (n_pair_heads < n_q_heads) {
-      const int rc = launch_sparse_attn(a, st);  // the other heads
+      // mixed layer: the union kernel runs anyway, so a listed head whose row blocks mostly
+      // share tiles (locality) stays on it; the per-head step counts decide (pair_preferred)
+      unsigned long long* stats = pair_stats_scratch(n_pair_heads);
+      if (stats == nullptr) return set_error(SPF_ERR_CUDA, "pair stats scratch allocation failed");
+      a.pair_stats = stats;
+      int rc = launch_pair_stats(a, stats, st);
+      if (rc) return rc;
+      rc = launch_sparse_attn(a, st);  // the other heads
       if (rc) return rc;
     }
     return launch_sparse_attn_pairs(a, st);

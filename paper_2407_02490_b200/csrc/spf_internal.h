@@ -36,12 +36,25 @@ struct AttnArgs {
   float* lse;                 // optional [Hq][S]: natural-log sum of exp(scale * q.k) over the row's cells
   const int32_t* pair_heads;  // optional device list of q-heads run by the paired-box kernel (attn_bs.cu)
   int n_pair;
+  // optional [n_pair][2]: per listed head, union steps and paired steps summed over its CTAs
+  // (pair_stats_kernel); a listed head whose row blocks mostly share tiles stays on the union
+  // kernel.  nullptr: every listed head runs the paired-box kernel.
+  const unsigned long long* pair_stats;
 };
+
+// The paired-box kernel pays ~1.6x a union step per step (N128 QK + K128 PV): it wins when the
+// CTAs' union steps exceed 1.6x their paired steps (measured: Block-Sparse on i.i.d. inputs,
+// union ~2x paired, pair 0.87x the union kernel's time; on locality inputs, union ~1.01x paired,
+// pair 1.49x).
+__host__ __device__ inline bool pair_preferred(const unsigned long long* stats, int i) {
+  return stats == nullptr || 5ull * stats[2 * i] > 8ull * stats[2 * i + 1];
+}
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
 // Paired-box kernel for heads whose row blocks rarely share tiles (attn_bs.cu).
 bool attn_pair_supported(const AttnArgs& a);
 int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream);
+int launch_pair_stats(const AttnArgs& a, unsigned long long* stats, cudaStream_t stream);
 // Two-tile (256-row) bf16 kernel, attn_fwd2.cu.
 bool attn2_supported(const AttnArgs& a);
 int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream);

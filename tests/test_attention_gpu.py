@@ -203,3 +203,42 @@ def test_pair_heads_validation(K):
         K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.float32, device=dev))
     out = K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.uint8, device=dev))
     assert out.abs().max().item() == 0  # no coverage -> zero rows; empty list = union kernel only
+
+
+def test_mixed_layer_routes_block_sparse_heads_by_overlap(K):
+    """A mixed layer (one unlisted head): listed heads whose row blocks share most tiles (a
+    locality band) stay on the union kernel, listed heads with scattered tiles run the
+    paired-box kernel (pair_stats_kernel decides on device); every head equals the oracle."""
+    hq, hkv, b, s, d = 4, 2, 64, 4096 + 64 * 7 + 9, 64
+    rng = np.random.Generator(np.random.PCG64(11))
+    q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    v = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    n = (s + b - 1) // b
+    kb = 24
+    tiles_all = []
+    for h in range(hq):
+        for r in range(n):
+            m = min(kb, r + 1)
+            if h in (0, 3):  # locality band: consecutive row blocks share all but one block
+                blocks = list(range(r - m + 1, r + 1))
+            else:  # scattered, diagonal forced
+                blocks = sorted(set([r] + rng.choice(r + 1, size=m, replace=False).tolist()))[-m:]
+                if r not in blocks:
+                    blocks[-1] = r
+            tiles_all.append(sorted(x * b for x in blocks))
+    ts, to = port.flatten(tiles_all)
+    co = np.zeros(hq * n + 1, np.int64)
+    dev = torch.device("cuda")
+    args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+            torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+            torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+            torch.zeros(1, dtype=torch.int32, device=dev), torch.from_numpy(co).to(dev))
+    got = K.sparse_flash_attention_gpu(*args, pair_heads=torch.tensor([0, 1, 3], dtype=torch.int32, device=dev))
+    got = got.float().cpu().numpy()
+    for h in range(hq):
+        kvh = h // (hq // hkv)
+        tt, tto = port.flatten(tiles_all[h * n:(h + 1) * n])
+        want = port.sparse_flash_rows(q[h], k[kvh], v[kvh], 1 / math.sqrt(d), b, tt, tto,
+                                      np.zeros(0, np.int64), np.zeros(n + 1, np.int64))
+        assert np.abs(got[h] - want).max() < BF16_TOL, (h, np.abs(got[h] - want).max())

@@ -80,8 +80,9 @@ int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const voi
  * estimator.estimate_block_sparse (estimator.py:117-143) -- which then run the
  * paired-box kernel: one step pairs the next tile of each of a CTA's two row blocks
  * (bf16, block_size 64, head_dim <= 128; otherwise the hint is ignored).  The count is
- * a host value, so a layer whose heads are all listed launches only that kernel.
- * Results follow the same contract. */
+ * a host value, so a layer whose heads are all listed launches only that kernel; in a
+ * mixed layer a listed head whose row blocks mostly share tiles (measured on the device
+ * from the CSR) stays on the union kernel.  Results follow the same contract. */
 int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
                              const int64_t* tile_offsets, const int32_t* col_indices, const int64_t* col_offsets,

@@ -161,19 +161,21 @@ def union_steps(tiles_np, toff_np, n_rows, hq, paired=None):
     counts = np.diff(toff_np)
     rows = np.repeat(np.arange(hq * n_rows, dtype=np.int64), counts)
     head = rows // n_rows
-    is_pair = np.zeros(hq, dtype=bool)
-    if paired is not None:
-        is_pair[np.asarray(paired, dtype=np.int64)] = True
-    keep = ~is_pair[head]
     pair = head * ((n_rows + 1) // 2) + (rows % n_rows) // 2
-    keys = pair[keep] * (np.int64(1) << 32) + tiles_np.astype(np.int64)[keep]
-    n_union = int(np.unique(keys).size)
-    n_paired = 0
-    for h in np.nonzero(is_pair)[0]:
+    keys = np.unique(pair * (np.int64(1) << 32) + tiles_np.astype(np.int64))
+    u_head = np.bincount(keys >> 32, minlength=hq * ((n_rows + 1) // 2)).reshape(hq, -1).sum(axis=1)
+    listed = [] if paired is None else [int(h) for h in np.asarray(paired).reshape(-1)]
+    n_union, n_paired = int(u_head.sum()), 0
+    for h in listed:
         c = counts[h * n_rows:(h + 1) * n_rows]
         if n_rows % 2:
             c = np.append(c, 0)
-        n_paired += int(np.maximum(c[0::2], c[1::2]).sum())
+        m = int(np.maximum(c[0::2], c[1::2]).sum())
+        # the library's routing (spf_internal.h pair_preferred): in a mixed layer a listed head
+        # stays on the union kernel unless its union steps exceed 1.6x its paired steps
+        if len(listed) == hq or 5 * int(u_head[h]) > 8 * m:
+            n_union -= int(u_head[h])
+            n_paired += m
     return n_union, n_paired
 
 

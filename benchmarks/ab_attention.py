@@ -29,6 +29,10 @@ n_pairs = [len(pair_ids) if os.environ.get(f"AB_PAIR_{x}", os.environ.get("AB_PA
 lay = P.build_layer_layout(q, k, cfgs, 64)
 out = torch.empty_like(q)
 vp = ctypes.c_void_p
+for lib in libs:
+    lib.spf_sparse_flash_workspace_size.restype = ctypes.c_size_t
+ws_bytes = max(int(lib.spf_sparse_flash_workspace_size(0, hq, 8, seq, 128)) for lib in libs)
+ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
 def run(lib, n_pair):
     lib.spf_sparse_flash_rows_ex.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_float, ctypes.c_int, vp, vp, vp, vp, vp,
@@ -37,7 +41,7 @@ def run(lib, n_pair):
                                       ctypes.c_float(128 ** -0.5), 64, vp(lay.tiles.data_ptr()),
                                       vp(lay.tile_offsets.data_ptr()), vp(lay.cols.data_ptr() if lay.cols.numel() else 0),
                                       vp(lay.col_offsets.data_ptr()), vp(pair.data_ptr()), n_pair, vp(out.data_ptr()), None,
-                                      None, 0, vp(torch.cuda.current_stream().cuda_stream))
+                                      vp(ws.data_ptr()), ws_bytes, vp(torch.cuda.current_stream().cuda_stream))
     assert rc == 0
 ts = [[], []]
 for r in range(int(os.environ.get("AB_REPS", "12"))):

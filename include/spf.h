@@ -58,6 +58,10 @@ unsigned long long spf_kernel_launches(void);
  *             SPF_DTYPE_F32 (fp32 in/out via bf16x2 split, the drop-in path)
  *   out     : [n_q_heads][seq_len][head_dim] of the same dtype
  *   head_dim: <= 128 (padded internally to 64/128 through the workspace)
+ * The workspace holds staged operand copies (fp32 split / padded head_dim; none for
+ * bf16 at head_dim 64 or 128) followed by 16 bytes per q-head of routing statistics
+ * used by spf_sparse_flash_rows_ex; a smaller workspace that still covers the copies
+ * is accepted (the statistics are then skipped).
  * ------------------------------------------------------------------------- */
 size_t spf_sparse_flash_workspace_size(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim);
 int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,

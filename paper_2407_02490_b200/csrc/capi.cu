@@ -106,13 +106,26 @@ unsigned long long spf_kernel_launches(void) { return __atomic_load_n(&spf::g_la
 
 static int padded_dim(int d) { return d <= 64 ? 64 : 128; }
 
-size_t spf_sparse_flash_workspace_size(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim) {
+}  // extern "C"
+
+namespace {
+// staged (split / padded) operand copies: 0 for bf16 inputs at head_dim 64 or 128
+size_t operand_bytes(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim) {
   const int kD = padded_dim(head_dim);
   const bool split = dtype == SPF_DTYPE_F32;
   if (!split && head_dim == kD) return 0;
   const size_t copies = split ? 2 : 1;
   const size_t per_head = (size_t)seq_len * kD * 2;
   return copies * (align256(per_head * n_q_heads) + 2 * align256(per_head * n_kv_heads));
+}
+}  // namespace
+
+extern "C" {
+
+// operand copies + the pair-routing statistics (two uint64 per q-head) after them
+size_t spf_sparse_flash_workspace_size(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim) {
+  return operand_bytes(dtype, n_q_heads, n_kv_heads, seq_len, head_dim) +
+         align256((size_t)(n_q_heads > 0 ? n_q_heads : 0) * 2 * sizeof(unsigned long long));
 }
 
 int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
@@ -132,30 +145,6 @@ int spf_sparse_flash_rows_lse(int dtype, const void* q, const void* k, const voi
                                   tile_starts, tile_offsets, col_indices, col_offsets, nullptr, 0, out, lse_out,
                                   workspace, workspace_bytes, stream);
 }
-
-}  // extern "C"
-
-namespace {
-// Per-device scratch for the routing statistics (grown on demand; cudaMalloc synchronises,
-// so it happens once per device in practice).
-unsigned long long* pair_stats_scratch(int n_pair) {
-  constexpr int kMaxDev = 64;
-  static unsigned long long* buf[kMaxDev] = {};
-  static int cap[kMaxDev] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
-  if (cap[dev] < n_pair) {
-    if (buf[dev] != nullptr) cudaFree(buf[dev]);
-    buf[dev] = nullptr;
-    const int want = n_pair < 256 ? 256 : n_pair;
-    if (cudaMalloc(&buf[dev], sizeof(unsigned long long) * 2 * want) != cudaSuccess) return nullptr;
-    cap[dev] = want;
-  }
-  return buf[dev];
-}
-}  // namespace
-
-extern "C" {
 
 int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
                              int seq_len, int head_dim, float scale, int block_size, const int32_t* tile_starts,
@@ -195,7 +184,7 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
   a.n_pair = 0;
   if (n_pair_heads < 0 || n_pair_heads > n_q_heads || (n_pair_heads > 0 && pair_heads == nullptr))
     return set_error(SPF_ERR_INVALID, "bad pair head list (%d heads)", n_pair_heads);
-  const size_t need = spf_sparse_flash_workspace_size(dtype, n_q_heads, n_kv_heads, seq_len, head_dim);
+  const size_t need = operand_bytes(dtype, n_q_heads, n_kv_heads, seq_len, head_dim);
   if (need == 0) {
     a.q_hi = q;
     a.k_hi = k;
@@ -243,12 +232,16 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
     if (n_pair_heads < n_q_heads) {
       // mixed layer: the union kernel runs anyway, so a listed head whose row blocks mostly
       // share tiles (locality) stays on it; the per-head step counts decide (pair_preferred)
-      unsigned long long* stats = pair_stats_scratch(n_pair_heads);
-      if (stats == nullptr) return set_error(SPF_ERR_CUDA, "pair stats scratch allocation failed");
-      a.pair_stats = stats;
-      int rc = launch_pair_stats(a, stats, st);
-      if (rc) return rc;
-      rc = launch_sparse_attn(a, st);  // the other heads
+      // (statistics live in the caller's workspace after the operand copies; without room for
+      // them every listed head runs the paired-box kernel)
+      const size_t stats_bytes = (size_t)n_pair_heads * 2 * sizeof(unsigned long long);
+      if (workspace != nullptr && workspace_bytes >= need + stats_bytes) {
+        unsigned long long* stats = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(workspace) + need);
+        a.pair_stats = stats;
+        const int rc = launch_pair_stats(a, stats, st);
+        if (rc) return rc;
+      }
+      const int rc = launch_sparse_attn(a, st);  // the other heads
       if (rc) return rc;
     }
     return launch_sparse_attn_pairs(a, st);

@@ -101,6 +101,21 @@ __device__ __forceinline__ uint32_t p_col(int t) { return kDB ? 384u + (uint32_t
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
+// SPF_PAIR_TRACE=1 (debug): clock64 stamps of softmax warp 2 (lane 0) per step in the union-pairing
+// path, 8 slots per (CTA, step), for the first spf_debug_pair_trace CTAs.
+#ifndef SPF_PAIR_TRACE
+#define SPF_PAIR_TRACE 0
+#endif
+constexpr int kPTraceSteps = 64;
+__device__ unsigned long long* g_ptrace = nullptr;
+__device__ int g_ptrace_ctas = 0;
+__device__ __forceinline__ void ptrace(bool on, int step, int ev) {
+  if (!SPF_PAIR_TRACE || !on) return;
+  unsigned long long* tr = g_ptrace;
+  if (tr == nullptr || (int)blockIdx.x >= g_ptrace_ctas || step >= kPTraceSteps) return;
+  tr[((int64_t)blockIdx.x * kPTraceSteps + step) * 8 + ev] = (unsigned long long)clock64();
+}
+
 template <int kD>
 __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -312,6 +327,8 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
       mbar_wait(&ctrl->d_full[sd], (t >> 1) & 1);
       const PairDesc& d = ctrl->desc[sd];
       if (d.end) break;
+      const bool tr0 = warp == 2 && lane == 0;
+      ptrace(tr0, t, 0);
       if (kUnion) {
         // both boxes may belong to this row's block: up to 128 keys per row
         int lo[2], hi[2];
@@ -332,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
         const bool warp_skip = !__any_sync(0xffffffffu, any);
         mbar_wait(&ctrl->s_full[t & 1], (t >> 1) & 1);
         tc_fence_after();
+        ptrace(tr0, t, 1);
         uint32_t x[kKeys];  // x[0, 64): this warp's own key half (box kh), x[64, 128): the other box
         float alpha = 1.f;
         bool rescale = false;
@@ -339,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
           tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + kh * kBox, x);
           tmem_ld32x32b_x64(tmem + lane_off + s_col(t) + (kh ^ 1) * kBox, x + kBox);
           tmem_wait_ld();
+          ptrace(tr0, t, 2);
           const int lo_a = kh ? lo[1] : lo[0], hi_a = kh ? hi[1] : hi[0];
           const int lo_b = kh ? lo[0] : lo[1], hi_b = kh ? hi[0] : hi[1];
           if (!(lo_a == 0 && hi_a == kBox)) {
@@ -358,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
             mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
           }
           const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+          ptrace(tr0, t, 3 + (__float_as_uint(mx) == 0x7fc00001u ? 1 : 0));
           if (any) {
             const float m_tile = mx * scale_log2;
             if (m_run == -INFINITY) {
@@ -389,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
             }
             x[j >> 1] = pack_bf16x2(p0, p1);
           }
+          ptrace(tr0, t, 4 + (__float_as_uint(x[0]) == 0x7fc00001u ? 1 : 0));
           float sa, sb;
           unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb);
           l_run = l_run * alpha + (sa + sb);
@@ -425,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, kDB ? 1 : 2)
           tmem_st32x32b_x32(tmem + lane_off + p_col(t) + kh * 32, x);  // P of this half's 64 keys
         }
         tmem_wait_st();
+        ptrace(tr0, t, 6);
         tc_fence_before();
         mbar_arrive(&ctrl->p_full[t & 1]);
         continue;
@@ -653,3 +675,10 @@ int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace spf
+
+// Debug: point the SPF_PAIR_TRACE stamps at a device buffer of n_ctas * 64 * 8 uint64.
+extern "C" int spf_debug_pair_trace(void* buf, int n_ctas) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  if (cudaMemcpyToSymbol(spf::g_ptrace, &p, sizeof(p)) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(spf::g_ptrace_ctas, &n_ctas, sizeof(int)) == cudaSuccess ? 0 : 1;
+}

@@ -134,7 +134,11 @@ def run_reference_arm(args, cfg):
               f"full index build, kernel on {args.ref_rows} sampled row blocks extrapolated by tiles+chips; "
               f"kernel = {'reference _core.pyx (oracle/_ref)' if info['ref_kernel'] else 'oracle port'}; "
               f"step latency = sum(item s)/cores")
-    line = {"impl": "reference", "metric": metric_name(args, cfg), "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus,
+    line = {"impl": "reference", "modeled": True,
+            "value_kind": (f"modeled: each step times a bounded sample ({info['items']} (layer, head) items; kernel on "
+                           f"{args.ref_rows} row blocks each) and extrapolates to the whole workload by tile count"),
+            "sample_items_per_step": info["items"],
+            "metric": metric_name(args, cfg), "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 3), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 storage)", "data": "synthetic (G-local)",
             "config": {"workload": cfg["workload"], "seq_len": cfg["seq_len"], "layers": cfg["layers"]},
@@ -171,68 +175,85 @@ def union_steps(tiles_np, toff_np, n_rows, hq, paired=None):
         if n_rows % 2:
             c = np.append(c, 0)
         m = int(np.maximum(c[0::2], c[1::2]).sum())
-        # the library's routing (spf_internal.h pair_preferred): in a mixed layer a listed head
-        # stays on the union kernel unless its union steps exceed 1.6x its paired steps
-        if len(listed) == hq or 5 * int(u_head[h]) > 8 * m:
+        # the library's routing (spf_internal.h pair_preferred): a listed head stays on the union
+        # kernel unless its union steps exceed 1.6x its paired steps (Block-Sparse heads have no
+        # residual columns, the other condition)
+        if 5 * int(u_head[h]) > 8 * m:
             n_union -= int(u_head[h])
             n_paired += m
     return n_union, n_paired
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--layers", type=int, default=None, help="override layer count (profiling only)")
-    ap.add_argument("--ref-rows", type=int, default=32)
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=0,
-                    help="head chunks (whole kv groups) per layer in the host-buffer pipeline of the e2e leg; "
-                         "0 = auto: 1 when the job has several layers (layer l+1's copy hides behind layer l), "
-                         "one per kv group for a single layer (C2 1 chunk 1115 ms vs 4: 1138; C4 1: 187 vs 8: 165)")
-    ap.add_argument("--shard", default="contiguous", choices=["contiguous", "lpt"],
-                    help="q-head partition over ranks: contiguous kv-group ranges, or LPT on modeled kernel FLOPs")
-    ap.add_argument("--gather", action="store_true",
-                    help="all-gather every layer's per-rank outputs into the full [Hq, S, d] on every rank "
-                         "(the optional collective of SURVEY 8e), inside the timed step")
-    args = ap.parse_args()
-    cfg = dict(CONFIGS[args.config])
-    if args.layers:
-        cfg["layers"] = args.layers
-    if args.warmup < 3:
-        args.warmup = 3
-    if args.impl == "reference":
-        return run_reference_arm(args, cfg)
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` launched directly (no WORLD_SIZE): re-exec under torchrun, one
+    rank per GPU, rendezvous on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
 
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # communicator setup lines (one per rank) on stderr, so stdout keeps the one JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, world, rank):
+    """CPU plumbing check of the multi-rank path (no GPU): gloo process group, the same
+    shard plan and max-over-ranks rule; each rank reports a synthetic per-rank time."""
+    import torch.distributed as dist
+
+    from paper_2407_02490_b200.sharding import max_over_ranks, shard_heads
+
+    cfg = CONFIGS[args.config]
+    if world > 1:
+        dist.init_process_group("gloo")
+    shard = shard_heads(cfg["hq"], cfg["hkv"], world, rank)
+    ms = max_over_ranks(1.0 + rank, device=None)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": metric_name(args, cfg), "value": ms, "unit": "ms",
+                          "n_gpus": world, "ms_per_step": ms, "rank0_q_heads": list(shard.q_heads)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def vs_bytes_min(cfgs_layer, S, D, HQ, HKV):
+    """SURVEY 8(d) algorithmic bytes of one layer's estimation (bf16, e = 2):
+    VS: K read once per kv head its VS heads use + the Q tail + the fp32 vertical/slash
+    vectors written and read back + the selected indices; BS: Q and K read once."""
+    from paper_2407_02490_b200.patterns import BlockSparse, VerticalSlash
+
+    e, hpk = 2, HQ // HKV
+    vs = [h for h, c in enumerate(cfgs_layer) if isinstance(c, VerticalSlash)]
+    bs = [h for h, c in enumerate(cfgs_layer) if isinstance(c, BlockSparse)]
+    out = 0
+    if vs:
+        kv = {h // hpk for h in vs}
+        out += len(kv) * S * D * e + sum(cfgs_layer[h].last_q for h in vs) * D * e + len(vs) * S * 4 * 2 * 2
+        out += sum(min(cfgs_layer[h].k_v, S) + min(cfgs_layer[h].k_s, S) for h in vs) * 4
+    if bs:
+        out += len(bs) * S * D * e + len({h // hpk for h in bs}) * S * D * e
+    return out
+
+
+def run_config(args, cfg, world, rank, local, dev, with_cpu, with_e2e, steps, label):
+    """Measure one workload: estimation + compaction + sparse attention for every layer
+    of this rank's heads, inputs resident in HBM.  Returns the per-config record."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     import paper_2407_02490_b200 as P
     from benchmarks.workloads import g_iid_qkv, g_local_qkv
     from paper_2407_02490_b200 import _lib, kernels
-    from paper_2407_02490_b200.patterns import AShape, BlockSparse, VerticalSlash
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+    from paper_2407_02490_b200.prefill import _pair_heads
+    from paper_2407_02490_b200.sharding import gather_heads, max_over_ranks, plan_heads_lpt, shard_heads
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # test hooks for exercising the multi-rank path on a one-GPU box: every rank on GPU 0,
-    # gloo for the barriers / max-reduction (the data path has no collective either way)
-    if os.environ.get("BENCH_SINGLE_DEVICE") == "1":
-        local = 0
-    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     S, HQ, HKV, L, D, B = cfg["seq_len"], cfg["hq"], cfg["hkv"], cfg["layers"], 128, 64
-    from paper_2407_02490_b200.sharding import max_over_ranks, plan_heads_lpt, shard_heads
-
     all_cfgs = layer_configs(cfg)[:L]
     if args.shard == "lpt":  # whole kv groups (or heads) balanced on the patterns' modeled kernel FLOPs
         from paper_2407_02490_b200.patterns import flops_in_kernel
@@ -246,8 +267,6 @@ def main():
     q_idx = torch.tensor(shard.q_heads, dtype=torch.long, device=dev)
     kv_idx = torch.tensor(shard.kv_stack, dtype=torch.long, device=dev)
     cfgs = [[row[h] for h in shard.q_heads] for row in all_cfgs]
-    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
-
     table = PatternTable(cfgs)  # this rank's heads; device head groups cached per layer
     gen = g_local_qkv if cfg["inputs"] == "G-local" else g_iid_qkv
 
@@ -263,25 +282,23 @@ def main():
     stream = torch.cuda.current_stream()
     scale = 1.0 / math.sqrt(D)
     lib = _lib.load()
-
-    attn_events = []
-    from paper_2407_02490_b200.sharding import gather_heads
-
-    from paper_2407_02490_b200.prefill import _pair_heads
-
-    pair_masks = [_pair_heads(cfgs[layer], dev) for layer in range(L)]  # Block-Sparse heads: paired-box kernel
+    pair_masks = [_pair_heads(cfgs[layer], dev) for layer in range(L)]  # Block-Sparse heads: paired-box candidates
+    est_events, attn_events = [], []
 
     def step(record=False):
         for layer in range(L):
+            if record:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
             lay = P.build_layer_layout(Q[layer], K[layer], cfgs[layer], B, groups=table.device_groups(layer, dev))
             if record:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+                e1.record(stream)
             kernels.sparse_flash_attention_gpu(Q[layer], K[layer], V[layer], scale, B, lay.tiles, lay.tile_offsets,
                                                lay.cols, lay.col_offsets, out=out, pair_heads=pair_masks[layer])
             if record:
-                e1.record(stream)
-                attn_events.append((e0, e1))
+                e2.record(stream)
+                est_events.append((e0, e1))
+                attn_events.append((e1, e2))
             if args.gather and world > 1:
                 gather_heads(out, shards)
 
@@ -289,12 +306,13 @@ def main():
     step()
     torch.cuda.synchronize()
     n_rows = (S + B - 1) // B
-    tiles_tot = chips_tot = union_tot = paired_tot = 0
+    tiles_tot = chips_tot = union_tot = paired_tot = cols_tot = 0
     area_tot = 0
     pattern_counts = {}
     for layer in range(L):
         lay = P.build_layer_layout(Q[layer], K[layer], cfgs[layer], B)
         tiles_tot += lay.n_tiles
+        cols_tot += lay.n_cols
         chips_tot += lay.chips()
         area_tot += int(lay.area().sum().item())
         plist = pair_masks[layer]
@@ -313,13 +331,15 @@ def main():
     clocks.start()
     time.sleep(0.3)
     if world > 1:
+        import torch.distributed as dist
+
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.spf_kernel_launches()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step(record=True)
     t1.record(stream)
     torch.cuda.synchronize()
@@ -328,10 +348,12 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     elapsed = max_over_ranks(t0.elapsed_time(t1), device=dev)
-    ms_per_step = elapsed / args.steps
+    ms_per_step = elapsed / steps
     attn_ms = [a.elapsed_time(b) for a, b in attn_events]
+    est_ms = [a.elapsed_time(b) for a, b in est_events]
     attn_avg = sum(attn_ms) / len(attn_ms)
-    attn_step_ms = sum(attn_ms) / args.steps
+    attn_step_ms = sum(attn_ms) / steps
+    est_step_ms = sum(est_ms) / steps
 
     # ---- roofline of the dominant kernel (sparse attention) ----
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
@@ -340,66 +362,159 @@ def main():
     achieved_tf = flops_issued_layer / (attn_avg * 1e-3) / 1e12
     # what the M=128 CTAs issue: union step = M128xN64 QK + K64 PV; paired step = N128 QK + K128 PV
     mma_flops_layer = (2 * tile_flops * (union_tot + chips_tot) + 4 * tile_flops * paired_tot) / L
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(REPO, "profiles", "attn_traffic.json")
-    if os.path.exists(tpath):
+    if world == 1 and os.path.exists(tpath):  # an ncu capture of this config's full-size (unsharded) launch
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+                rec = json.load(f).get(label, {})
+            traffic, traffic_src = rec.get("dram_bytes_per_launch"), rec.get("source")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": tf_sust, "unit": "TFLOP/s",
                 "frac": round(achieved_tf / tf_sust, 4), "traffic": traffic,
+                "traffic_source": traffic_src if traffic is not None else
+                ("omitted: sharded run (the ncu capture is of the full unsharded launch)" if world > 1 else None),
+                "frac_of_burst_peak": round(achieved_tf / tf_burst, 4),
                 "kernel": ("sparse_attn_pair_kernel<128>" if union_tot + chips_tot == 0 else
                            "sparse_attn_fwd_kernel<128,false>" + (" + sparse_attn_pair_kernel<128>" if paired_tot else "")),
-                "peak_source": f"{peak_src} bf16 sustained",
+                "peak_source": f"{peak_src} bf16 sustained (burst {tf_burst})",
                 "flops_per_launch": flops_issued_layer, "avg_launch_ms": round(attn_avg, 4),
                 "mma_flops_per_launch": mma_flops_layer,
                 "mma_frac": round(mma_flops_layer / (attn_avg * 1e-3) / 1e12 / tf_sust, 4),
                 "attn_share_of_step": round(attn_step_ms / ms_per_step, 4)}
+    # ---- estimation + compaction against the HBM roofline (SURVEY 8d "HBM fraction") ----
+    bmin = sum(vs_bytes_min(cfgs[layer], S, D, hq_loc, len(set(shard.kv_stack))) for layer in range(L))
+    csr_bytes = 4 * (tiles_tot + cols_tot) + L * 2 * 8 * (hq_loc * n_rows + 1)
+    est_roof = {"bound": "hbm", "bytes_min_per_step": int(bmin), "csr_bytes_per_step": int(csr_bytes),
+                "ms_per_step": round(est_step_ms, 3), "ms_per_layer": round(est_step_ms / L, 4),
+                "achieved_gbs": round(bmin / (est_step_ms * 1e-3) / 1e9, 1) if est_step_ms > 0 else None,
+                "peak_gbs": hbm, "frac": round(bmin / (est_step_ms * 1e-3) / 1e9 / hbm, 4) if est_step_ms > 0 else None,
+                "note": "CUDA events around build_layer_layout (estimation, certification / exact fp64 path, "
+                        "index compaction, CSR sizing) on the launch stream; bytes_min per SURVEY 8(d)"}
 
-    # ---- end to end through the public API with host buffers ----
     e2e = None
-    if not args.no_e2e:
+    if with_e2e:
         e2e = run_e2e(args, SparsePrefill(table, B), torch, Q, K, V, L, stream)
         e2e["value"] = round(max_over_ranks(e2e["value"], device=dev), 3)
 
-    # ---- dense FlashAttention-class baseline (torch SDPA, bf16, causal, GQA), one layer ----
     dense = None
     if rank == 0 and not args.no_dense:
         dense = dense_baseline(torch, Q[0], K[0], V[0], L, ms_per_step)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and with_cpu:
         cpu = cpu_baseline(cfg, all_cfgs)
 
+    sparsity = 1.0 - area_tot / (L * hq_loc * S * (S + 1) / 2)
+    rec = {
+        "value": round(ms_per_step, 3), "ms_per_step": round(ms_per_step, 3), "steps": steps,
+        "config": {"workload": cfg["workload"], "seq_len": S, "layers": L, "q_heads": HQ, "kv_heads": HKV,
+                   "head_dim": D, "block_size": B, "patterns": cfg["patterns"],
+                   "pattern_heads_this_rank": pattern_counts, "inputs": cfg["inputs"] + " (SURVEY.md 8d)",
+                   "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush" % (
+                       sum(t.numel() * 2 for t in Q + K + V) / 1e9),
+                   "parallelism": (f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
+                                   f"divides {HKV}), no data-path collective" if args.shard == "contiguous" else
+                                   f"q-heads sharded over {world} GPU(s) by LPT on modeled kernel FLOPs (whole kv "
+                                   f"groups when {world} <= {HKV}), no data-path collective"),
+                   "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
+                   "union_steps": union_tot, "paired_steps": paired_tot,
+                   "output_all_gather": bool(args.gather and world > 1)},
+        "roofline": roofline,
+        "estimate_roofline": est_roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk,
+        "gpu_launches": int(launches),
+        "attention_ms_per_step": round(attn_step_ms, 3),
+        "estimate_index_ms_per_step": round(est_step_ms, 3),
+        "dense_baseline": dense,
+    }
+    del Q, K, V, out
+    torch.cuda.empty_cache()
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--layers", type=int, default=None, help="override layer count (profiling only)")
+    ap.add_argument("--ref-rows", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the 1M Vertical-Slash sub-record of the C2 line")
+    ap.add_argument("--dry-run", action="store_true", help="CPU plumbing check of the rank launch (gloo, no GPU)")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="head chunks (whole kv groups) per layer in the host-buffer pipeline of the e2e leg; "
+                         "0 = auto: 1 when the job has several layers (layer l+1's copy hides behind layer l), "
+                         "one per kv group for a single layer (C2 1 chunk 1115 ms vs 4: 1138; C4 1: 187 vs 8: 165)")
+    ap.add_argument("--shard", default="contiguous", choices=["contiguous", "lpt"],
+                    help="q-head partition over ranks: contiguous kv-group ranges, or LPT on modeled kernel FLOPs")
+    ap.add_argument("--gather", action="store_true",
+                    help="all-gather every layer's per-rank outputs into the full [Hq, S, d] on every rank "
+                         "(the optional collective of SURVEY 8e), inside the timed step")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.layers:
+        cfg["layers"] = args.layers
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        return dry_run(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    # test hooks for exercising the multi-rank path on a one-GPU box: every rank on GPU 0,
+    # gloo for the barriers / max-reduction (the data path has no collective either way)
+    if os.environ.get("BENCH_SINGLE_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
+
+    rec = run_config(args, cfg, world, rank, local, dev, with_cpu=not args.no_cpu, with_e2e=not args.no_e2e,
+                     steps=args.steps, label=args.config)
+    c3 = None
+    if args.config == "c2" and not args.no_c3 and not args.layers:
+        # the 1M Vertical-Slash headline (C3) in the same run, sharded the same way
+        c3cfg = dict(CONFIGS["c3"])
+        c3 = run_config(args, c3cfg, world, rank, local, dev, with_cpu=False, with_e2e=not args.no_e2e,
+                        steps=min(args.steps, 5), label="c3")
+        c3 = {"metric": metric_name(argparse.Namespace(config="c3"), c3cfg), "unit": "ms", **c3}
+        if c3.get("dense_baseline") and "ms_per_layer" in c3["dense_baseline"]:
+            c3["speedup_vs_dense_device"] = round(c3["dense_baseline"]["ms_per_layer"] / c3["ms_per_step"], 2)
+            if c3.get("e2e"):
+                c3["speedup_vs_dense_e2e"] = round(c3["dense_baseline"]["ms_per_layer"] / c3["e2e"]["value"], 2)
+
     if rank == 0:
-        sparsity = 1.0 - area_tot / (L * hq_loc * S * (S + 1) / 2)
-        line = {
-            "metric": metric_name(args, cfg),
-            "value": round(ms_per_step, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "seq_len": S, "layers": L, "q_heads": HQ, "kv_heads": HKV,
-                       "head_dim": D, "block_size": B, "patterns": cfg["patterns"],
-                       "pattern_heads_this_rank": pattern_counts, "inputs": cfg["inputs"] + " (SURVEY.md 8d)",
-                       "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush" % (
-                           sum(t.numel() * 2 for t in Q + K + V) / 1e9),
-                       "parallelism": (f"q-heads sharded over {world} GPU(s) (whole kv groups when {world} "
-                                       f"divides {HKV}), no data-path collective" if args.shard == "contiguous" else
-                                       f"q-heads sharded over {world} GPU(s) by LPT on modeled kernel FLOPs (whole kv "
-                                       f"groups when {world} <= {HKV}), no data-path collective"),
-                       "realized_kernel_sparsity": round(sparsity, 4), "tiles": tiles_tot, "column_chips": chips_tot,
-                       "union_steps": union_tot, "paired_steps": paired_tot, "output_all_gather": bool(args.gather and world > 1)},
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "clocks": clk,
-            "gpu_launches": int(launches),
-            "attention_ms_per_step": round(attn_step_ms, 3),
-            "estimate_index_ms_per_step": round(ms_per_step - attn_step_ms, 3),
-            "dense_baseline": dense,
-        }
+        line = {"metric": metric_name(args, cfg), "value": rec["value"], "unit": "ms", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic"}
+        line.update({k: v for k, v in rec.items() if k not in ("value", "ms_per_step", "steps")})
+        if c3 is not None:
+            line["c3_1m"] = c3
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

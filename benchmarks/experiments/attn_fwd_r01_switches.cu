@@ -61,18 +61,39 @@ struct StepDesc {
 template <bool kSplit>
 constexpr bool kSepP = !kSplit;
 
-// One softmax warp per TMEM lane quarter (two, each exponentiating half a row, was
-// measured 14 % slower on C2: more warps per SMSP delay the MMA and loader warps more
-// than the shorter softmax helps).
+// softmax warps per TMEM lane quarter.  2 (each thread exponentiates half a row, both
+// halves read the whole row for the max) was measured 14% slower than 1 on C2: more
+// warps per SMSP delay the MMA and loader warps more than the shorter softmax helps.
+#ifndef SPF_SOFT_HALVES
+#define SPF_SOFT_HALVES 1
+#endif
 template <bool kSplit>
-constexpr int kSoftHalves = 1;
+constexpr int kSoftHalves = kSplit ? 1 : SPF_SOFT_HALVES;
 template <bool kSplit>
 constexpr int kThreadsT = 64 + 128 * kSoftHalves<kSplit>;
 
 template <bool kSplit>
 struct Rings {
-  static constexpr int kK = kSplit ? 2 : 3;
-  static constexpr int kV = 2;
+#ifndef SPF_P_EARLY
+#define SPF_P_EARLY 0  // 1: P(t) stored to TMEM before the row sum / O rescale
+#endif
+#ifndef SPF_DESC_UNDER_LD
+#define SPF_DESC_UNDER_LD 1  // row ranges from the step descriptor computed under the S load (0.1-0.2 %)
+#endif
+#ifndef SPF_MIN_SMEM
+#define SPF_MIN_SMEM 0
+#endif
+#ifndef SPF_KV_MAJOR
+#define SPF_KV_MAJOR 0  // kv-head-major item order: 0.7-1.1 % slower on C2-shaped VS / A-shape layers
+#endif
+#ifndef SPF_RING_K
+#define SPF_RING_K 3
+#endif
+#ifndef SPF_RING_V
+#define SPF_RING_V 2
+#endif
+  static constexpr int kK = kSplit ? 2 : SPF_RING_K;
+  static constexpr int kV = kSplit ? 2 : SPF_RING_V;
   static constexpr int kD = 3;  // step descriptors: written with K (one step ahead), freed by the softmax
 };
 
@@ -119,6 +140,30 @@ struct Layout {
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
+// Debug timeline (spf_debug_attn_trace): per traced CTA, 4 slots per (role, step):
+// role 0 = MMA warp, 1 = softmax warp 2.
+constexpr int kTraceSteps1 = 64;
+__device__ unsigned long long* g_trace1 = nullptr;
+__device__ int g_trace1_ctas = 0;
+// Bottleneck experiments (timing only, results are garbage): 1 = synthetic loader
+// schedule without list reads, 2 = softmax skipped, 3 = QK MMAs skipped, 4 = PV MMAs skipped,
+// 5 = K/V tile loads skipped (barriers still flip), 6 = 2 + 5.
+#ifndef SPF_EXPT
+#define SPF_EXPT 0
+#endif
+#ifndef SPF_TRACE
+#define SPF_TRACE 0
+#endif
+__device__ __forceinline__ void trace1(int role, int step, int ev) {
+  if (!SPF_TRACE) return;
+  unsigned long long* tr = g_trace1;
+  if (tr == nullptr || (int)blockIdx.x >= g_trace1_ctas || step >= kTraceSteps1) return;
+  unsigned long long t;
+  if (SPF_TRACE == 3) t = (unsigned long long)clock64();  // cycles (same SM throughout)
+  else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[(((int64_t)blockIdx.x * 3 + role) * kTraceSteps1 + step) * 4 + ev] = t;
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]: P (bf16, K-major, 2 per 32-bit column) times V.
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -155,14 +200,21 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- work item: heavy (late) row tiles first, heads fastest (a kv-head-major order, as the
-  // paired-box kernel uses for the scattered Block-Sparse tiles, measured 0.7-1.1 % slower on
-  // C2-shaped VS / A-shape layers: their K/V windows are local) ----------------------------
+  // ---- work item: heavy (late) row tiles first, heads fastest (SPF_KV_MAJOR: kv-head major,
+  // as the paired-box kernel does for the scattered Block-Sparse tiles) ---------------------
   int item = blockIdx.x;
   if (p.work_order != nullptr) item = p.work_order[item];
+#if SPF_KV_MAJOR
+  const int hpk = p.Hq / p.Hkv;
+  const int kvh = item / (n_ctile * hpk);
+  const int rem = item - kvh * (n_ctile * hpk);
+  const int ct = n_ctile - 1 - rem / hpk;
+  const int h = kvh * hpk + rem % hpk;
+#else
   const int ct = n_ctile - 1 - item / p.Hq;
   const int h = item % p.Hq;
   const int kvh = h / (p.Hq / p.Hkv);
+#endif
   for (int i = 0; i < p.n_pair; ++i)
     if (p.pair_heads[i] == h) {
       if (pair_preferred(p.pair_stats, i)) return;  // run by the paired-box kernel (attn_bs.cu)
@@ -267,7 +319,19 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       c0 = p.col_offsets[row0];
       cend = p.col_offsets[row0 + 1];
     }
+    int expt_left = (SPF_EXPT == 1 && G > 0) ? (int)(p.tile_offsets[row0 + 1] - p.tile_offsets[row0]) : 0;
     auto next_step = [&](StepInfo& st) {
+      if (SPF_EXPT == 1) {
+        if (expt_left-- > 0) {
+          st.kind = kTile;
+          st.box = max(0, R0 + kRows - kBox - kBox * expt_left);
+          st.width = kBox;
+          st.mask = ~0ull;
+        } else {
+          st.kind = kEnd;
+        }
+        return;
+      }
       if (phase == 0) {
         if (!tile_open) {
           const int best = __reduce_max_sync(0xffffffffu, max(cur[0], cur[1]));
@@ -398,7 +462,9 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       uint8_t* kst = smem + L::kOffK + sk * (L::kCopies * L::kKBytes);
       if (lane == 0) mbar_wait(&ctrl->k_empty[sk], ((t / R::kK) & 1) ^ 1);
       __syncwarp();
-      if (st.kind == kTile) {
+      if (st.kind == kTile && (SPF_EXPT == 5 || SPF_EXPT == 6)) {
+        if (lane == 0) mbar_arrive(&ctrl->k_full[sk]);
+      } else if (st.kind == kTile) {
         if (lane == 0) {
           mbar_arrive_expect_tx(&ctrl->k_full[sk], L::kTxKV);
 #pragma unroll
@@ -423,6 +489,8 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       if (st.kind == kChip) {
         gather(vst, vb, vb2, st);
         if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
+      } else if (SPF_EXPT == 5 || SPF_EXPT == 6) {
+        if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
       } else if (lane == 0) {
         mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
 #pragma unroll
@@ -438,14 +506,27 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     StepInfo pend;
     bool have_pend = false;
     int t = 0;
+    long long tl_gen = 0, tl_k = 0, tl_v = 0;
     while (true) {
       StepInfo st;
+      long long c0 = SPF_TRACE ? clock64() : 0;
       next_step(st);
+      long long c1 = SPF_TRACE ? clock64() : 0;
       if (st.kind != kEnd) issue_k(have_pend ? t + 1 : t, st);
       else write_desc(have_pend ? t + 1 : t, st);  // end marker through the descriptor ring
+      long long c2 = SPF_TRACE ? clock64() : 0;
       if (have_pend) {
         issue_v(t, pend);
         ++t;
+      }
+      if (SPF_TRACE) {
+        tl_gen += c1 - c0;
+        tl_k += c2 - c1;
+        tl_v += clock64() - c2;
+        if (lane == 0 && t == 48 && g_trace1 != nullptr && (int)blockIdx.x < g_trace1_ctas) {
+          unsigned long long* tr = g_trace1 + (((int64_t)blockIdx.x * 3 + 2) * kTraceSteps1 + 60) * 4;
+          tr[0] = tl_gen; tr[1] = tl_k; tr[2] = tl_v;
+        }
       }
       if (st.kind == kEnd) break;
       pend = st;
@@ -470,13 +551,14 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       auto issue_pv = [&](int u) {
         const int sv = u % R::kV;
         mbar_wait(&ctrl->p_full[u & 1], (u >> 1) & 1);
+        if (lane == 0) trace1(0, u, 2);
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
         tc_fence_after();
         const uint32_t vd = vlo0 + ((sv * kStageKV) >> 4);
         // P(u): own columns (separate-P) or over S(u) (split: hi in cols 0..31, lo in 32..63)
         const uint32_t tP = kSepP<kSplit> ? tmem + kBox + (u & 1) * (kBox / 2) : tmem + (u & 1) * kBox;
 #pragma unroll
-        for (int k = 0; k < kBox / 16; ++k) {
+        for (int k = 0; k < (SPF_EXPT == 4 ? 0 : kBox / 16); ++k) {
           const uint32_t b_hi = vd + ((k * 2048) >> 4);
           mma_bf16_ts_w2(tO, tP + k * 8, b_hi, dhi, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
           if (kSplit) {
@@ -504,10 +586,12 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           mbar_wait(&ctrl->s_free[sb], ((t >> 1) & 1) ^ 1);
         }
         tc_fence_after();
+        if (lane == 0) trace1(0, t, 0);
         const uint32_t kd = klo0 + ((sk * kStageKV) >> 4);
         const uint32_t tS = tmem + sb * kBox;
+        const long long c_qk0 = SPF_TRACE ? clock64() : 0;
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
+        for (int k = 0; k < (SPF_EXPT == 3 ? 0 : kD / 16); ++k) {
           const uint32_t aoff = ((k >> 2) * (kRows * 128) + (k & 3) * 32) >> 4;
           const uint32_t boff = ((k >> 2) * (kBox * 128) + (k & 3) * 32) >> 4;
           mma_bf16_ss_w2(tS, qlo0 + aoff, dhi, kd + boff, dhi, idesc_qk, k > 0 ? 1u : 0u);
@@ -518,7 +602,14 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         }
         mma_commit_w(&ctrl->s_full[sb]);
         mma_commit_w(&ctrl->k_empty[sk]);
+        if (SPF_TRACE && lane == 0) {
+          trace1(0, t, 1);
+          const long long dc = clock64() - c_qk0;
+          if (g_trace1 != nullptr && (int)blockIdx.x < g_trace1_ctas && t < kTraceSteps1)
+            g_trace1[(((int64_t)blockIdx.x * 3 + 2) * kTraceSteps1 + t) * 4 + 0] = (unsigned long long)dc;
+        }
         if (t > 0) issue_pv(t - 1);
+        if (lane == 0 && t > 0) trace1(0, t - 1, 3);
       }
       if (t > 0) issue_pv(t - 1);
       mma_commit_w(&ctrl->o_ready);
@@ -546,7 +637,10 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     int t = 0;
     for (;; ++t) {
       const int sd = t % R::kD;
+      const bool tr0 = warp == 2 && lane == 0;
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 0);
       mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 1);
       const StepDesc& d = ctrl->desc[sd];
       const int kind = d.kind;
       if (kind == kEnd) break;
@@ -557,6 +651,17 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
       }
       tc_fence_after();
+      if (tr0 && SPF_TRACE != 3) trace1(1, t, 2);
+      // lag 2: P buffer t&1 was last read by PV(t-2); S(t) ready only implies PV(t-3) retired
+      if (SPF_EXPT == 2 || SPF_EXPT == 6) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);
+        if (kSepP<kSplit> && lane == 0) mbar_arrive(&ctrl->s_free[0]);
+        l_run = 1.f;
+        tc_fence_before();
+        mbar_arrive(&ctrl->p_full[sb]);
+        continue;
+      }
       const uint32_t s_col = kSepP<kSplit> ? 0u : (uint32_t)(sb * kBox);
       uint32_t x[kCols];                          // own keys c0 .. c0+kCols-1
       uint32_t y[kHalves > 1 ? kBox - kCols : 1];  // the other half (max only)
@@ -566,6 +671,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         tmem_ld32x32b_x32(tmem + lane_off + s_col + c0, x);
         tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
       }
+#if SPF_DESC_UNDER_LD
       // valid key slots for this row, [lo, hi), computed while the TMEM load is in flight
       int lo = 0, hi = 0;
       if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
@@ -583,12 +689,33 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+#endif
       tmem_wait_ld();
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, 0);
       if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctrl->s_free[0]);
       }
+#if !SPF_DESC_UNDER_LD
+      // valid key slots for this row: a contiguous range [lo, hi)
+      int lo = 0, hi = 0;
+      if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
+        if (kind == kTile) {
+          lo = max(0, -d.box);
+          hi = min(d.width, min(S - d.box, q - d.box + 1));
+        } else {
+          int a = 0, b = d.width;
+          while (a < b) {
+            const int m = (a + b) >> 1;
+            if (d.pmax[m] <= q) a = m + 1; else b = m;
+          }
+          hi = a;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+#endif
       if (!__any_sync(0xffffffffu, hi > lo)) {
         // none of this warp's rows sees the step (the other row block's tile of a union
         // step, a block-sparse block of the other row): P = 0, softmax state unchanged
@@ -638,6 +765,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         }
       }
       const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, __float_as_int(mx) == 0x7fc00001 ? 0 : 1);  // after the max
       float alpha = 1.f;
       bool rescale = false;
       if (hi > lo) {
@@ -678,6 +806,19 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           pl[j >> 1] = pack_bf16x2(p0 - hf.x, p1 - hf.y);
         }
       }
+      if (tr0 && SPF_TRACE == 3) trace1(1, t, 2);  // after the exponentials
+#if SPF_P_EARLY
+      // P(t) -> TMEM right away (its buffer was last read by PV(t-2), retired once S(t) was
+      // ready); the row sum and an O rescale proceed while the store drains
+      if (kSepP<kSplit>) {
+        const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
+        if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);
+        else tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
+      } else {
+        tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
+        if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      }
+#endif
       float sa, sb2;
       unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
       const float sum = sa + sb2;
@@ -702,6 +843,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           tmem_st32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
         }
       }
+#if !SPF_P_EARLY
       // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
       if (kSepP<kSplit>) {
         const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
@@ -711,9 +853,11 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
         if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
       }
+#endif
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ctrl->p_full[sb]);
+      if (tr0) trace1(1, t, 3);
     }
     // ---- epilogue: O / l -> global ----
     if (t > 0) {
@@ -810,7 +954,9 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
     tv2 = tv;
   }
   auto kern = sparse_attn_fwd_kernel<kD, kSplit>;
-  constexpr int kLaunchSmem = L::kSmem;
+  // SPF_MIN_SMEM (experiment knob, default 0): launch with at least this much dynamic shared
+  // memory, e.g. 120000 to hold the kernel to one CTA per SM
+  constexpr int kLaunchSmem = L::kSmem > SPF_MIN_SMEM ? L::kSmem : SPF_MIN_SMEM;
   static bool attr_done = false;  // per template instance
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaunchSmem);
@@ -829,9 +975,21 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
+int attn1_set_trace(unsigned long long* buf, int n_ctas) {
+  int rc = check_cuda(cudaMemcpyToSymbol(g_trace1, &buf, sizeof(buf)), "trace ptr");
+  if (rc) return rc;
+  return check_cuda(cudaMemcpyToSymbol(g_trace1_ctas, &n_ctas, sizeof(int)), "trace ctas");
+}
+
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream) {
   if (a.B < 2) return set_error(2, "block_size must be >= 2 for the sm_100a kernel (got %d)", a.B);
   if (a.Hkv <= 0 || a.Hq % a.Hkv != 0) return set_error(2, "n_q_heads must be a multiple of n_kv_heads");
+  static const int kernel_choice = [] {
+    const char* e = getenv("SPF_ATTN_KERNEL");
+    return e ? atoi(e) : 1;
+  }();
+  if (kernel_choice == 2 && a.lse == nullptr && a.pair_heads == nullptr && attn2_supported(a))
+    return launch_sparse_attn2(a, stream);
   if (a.kD == 128) return a.split ? launch_impl<128, true>(a, stream) : launch_impl<128, false>(a, stream);
   if (a.kD == 64) return a.split ? launch_impl<64, true>(a, stream) : launch_impl<64, false>(a, stream);
   return set_error(2, "padded head_dim must be 64 or 128 (got %d)", a.kD);

@@ -30,15 +30,19 @@ def stream_handle(stream=None):
 _ws_cache: dict = {}
 
 
-def workspace(nbytes: int, device) -> torch.Tensor | None:
-    """Per-device grow-only scratch buffer (stream-ordered reuse)."""
+def workspace(nbytes: int, device, stream=None) -> torch.Tensor | None:
+    """Grow-only scratch buffer per (device, stream): work ordered on one stream reuses
+    it in stream order, and two streams never share one (include/spf.h: the library is
+    re-entrant per stream with caller-owned workspaces)."""
     if nbytes <= 0:
         return None
     dev = torch.device(device)
-    key = (dev.type, dev.index)
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    key = (dev.type, dev.index, int(s.cuda_stream))
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(s):  # owned by (allocated on) the stream that uses it
+            buf = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
         _ws_cache[key] = buf
     return buf
 

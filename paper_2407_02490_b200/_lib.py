@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SPF_LIB_OVERRIDE") or os.path.join(_PKG, "libspf.so")  # override: experiment builds
+LIB_PATH = os.path.join(_PKG, "libspf.so")
 
 SPF_DTYPE_BF16 = 0
 SPF_DTYPE_F32 = 1

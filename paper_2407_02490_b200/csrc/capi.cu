@@ -122,10 +122,10 @@ size_t operand_bytes(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int 
 
 extern "C" {
 
-// operand copies + the pair-routing statistics (two uint64 per q-head) after them
+// operand copies + the pair-routing statistics (kPairStatWords uint64 per q-head) after them
 size_t spf_sparse_flash_workspace_size(int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim) {
   return operand_bytes(dtype, n_q_heads, n_kv_heads, seq_len, head_dim) +
-         align256((size_t)(n_q_heads > 0 ? n_q_heads : 0) * 2 * sizeof(unsigned long long));
+         align256((size_t)(n_q_heads > 0 ? n_q_heads : 0) * kPairStatWords * sizeof(unsigned long long));
 }
 
 int spf_sparse_flash_rows(int dtype, const void* q, const void* k, const void* v, int n_q_heads, int n_kv_heads,
@@ -227,23 +227,19 @@ int spf_sparse_flash_rows_ex(int dtype, const void* q, const void* k, const void
     a.v_lo = vl;
   }
   if (n_pair_heads > 0 && attn_pair_supported(a)) {
+    // every listed head is routed by its measured statistics (pair_stats_kernel, in the
+    // caller's workspace after the operand copies); the union kernel runs all other heads
+    const size_t stats_bytes = (size_t)n_pair_heads * kPairStatWords * sizeof(unsigned long long);
+    if (workspace == nullptr || workspace_bytes < need + stats_bytes)
+      return set_error(SPF_ERR_INVALID, "workspace too small for the pair-routing statistics (%zu < %zu bytes)",
+                       workspace_bytes, need + stats_bytes);
+    unsigned long long* stats = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(workspace) + need);
     a.pair_heads = pair_heads;
     a.n_pair = n_pair_heads;
-    if (n_pair_heads < n_q_heads) {
-      // mixed layer: the union kernel runs anyway, so a listed head whose row blocks mostly
-      // share tiles (locality) stays on it; the per-head step counts decide (pair_preferred)
-      // (statistics live in the caller's workspace after the operand copies; without room for
-      // them every listed head runs the paired-box kernel)
-      const size_t stats_bytes = (size_t)n_pair_heads * 2 * sizeof(unsigned long long);
-      if (workspace != nullptr && workspace_bytes >= need + stats_bytes) {
-        unsigned long long* stats = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(workspace) + need);
-        a.pair_stats = stats;
-        const int rc = launch_pair_stats(a, stats, st);
-        if (rc) return rc;
-      }
-      const int rc = launch_sparse_attn(a, st);  // the other heads
-      if (rc) return rc;
-    }
+    a.pair_stats = stats;
+    int rc = launch_pair_stats(a, stats, st);
+    if (rc) return rc;
+    if ((rc = launch_sparse_attn(a, st))) return rc;
     return launch_sparse_attn_pairs(a, st);
   }
   return launch_sparse_attn(a, st);

@@ -245,10 +245,7 @@ __global__ void pool_vec_kernel(const T* __restrict__ x, int64_t n_heads, int S,
                              __double2float_rn(acc[j + 2] / len), __double2float_rn(acc[j + 3] / len));
 }
 
-#ifndef SPF_BS_ROW_THREADS
-#define SPF_BS_ROW_THREADS 256
-#endif
-constexpr int kBsThreads = SPF_BS_ROW_THREADS;
+constexpr int kBsThreads = 256;  // 128 measured 2 % slower on C4
 
 // One CTA per (head, block row r): block-causal softmax of the pooled scores
 // (fp64, rounded to fp32), top-min(k_b, r+1) with the diagonal forced.  The row's

@@ -36,18 +36,23 @@ struct AttnArgs {
   float* lse;                 // optional [Hq][S]: natural-log sum of exp(scale * q.k) over the row's cells
   const int32_t* pair_heads;  // optional device list of q-heads run by the paired-box kernel (attn_bs.cu)
   int n_pair;
-  // optional [n_pair][2]: per listed head, union steps and paired steps summed over its CTAs
-  // (pair_stats_kernel); a listed head whose row blocks mostly share tiles stays on the union
-  // kernel.  nullptr: every listed head runs the paired-box kernel.
+  // [n_pair][kPairStatWords]: per listed head, union steps, paired steps and residual columns
+  // summed over its CTAs (pair_stats_kernel); every listed head is routed by them.
   const unsigned long long* pair_stats;
 };
+
+constexpr int kPairStatWords = 3;
 
 // The paired-box kernel pays ~1.6x a union step per step (N128 QK + K128 PV): it wins when the
 // CTAs' union steps exceed 1.6x their paired steps (measured: Block-Sparse on i.i.d. inputs,
 // union ~2x paired, pair 0.87x the union kernel's time; on locality inputs, union ~1.01x paired,
-// pair 1.49x).
+// pair 1.49x).  It has no column-chip path, so a head with residual columns never goes there.
+// The union kernel runs every head the paired-box kernel does not (its CTAs of the others
+// exit at once), so coverage never depends on the list: duplicate or out-of-range ids
+// cannot leave a head unwritten.
 __host__ __device__ inline bool pair_preferred(const unsigned long long* stats, int i) {
-  return stats == nullptr || 5ull * stats[2 * i] > 8ull * stats[2 * i + 1];
+  const unsigned long long* s = stats + kPairStatWords * i;
+  return s[2] == 0 && 5ull * s[0] > 8ull * s[1];
 }
 
 int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
@@ -55,9 +60,6 @@ int launch_sparse_attn(const AttnArgs& a, cudaStream_t stream);
 bool attn_pair_supported(const AttnArgs& a);
 int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream);
 int launch_pair_stats(const AttnArgs& a, unsigned long long* stats, cudaStream_t stream);
-// Two-tile (256-row) bf16 kernel, attn_fwd2.cu.
-bool attn2_supported(const AttnArgs& a);
-int launch_sparse_attn2(const AttnArgs& a, cudaStream_t stream);
 
 // fp64 Vertical-Slash estimation (estimate_vs_exact.cu): all heads (gate == nullptr) or the
 // flagged ones; tile_max / row_mc (from the tensor-core pass, last_q 64) enable exact tile skipping.

@@ -34,10 +34,7 @@ struct BlockTopK {
   using Key = typename std::conditional<sizeof(T) == 8, uint64_t, uint32_t>::type;
   // 8-bit digits: a 256-bin histogram is zeroed and scanned with one bin per thread (rows
   // of a few thousand candidates pay more for 2048-bin rounds than for one extra round)
-#ifndef SPF_TOPK_BITS32
-#define SPF_TOPK_BITS32 8
-#endif
-  static constexpr int kBits = sizeof(T) == 4 ? SPF_TOPK_BITS32 : 8;
+  static constexpr int kBits = 8;  // 11-bit digits for fp32 keys (3 rounds) measured 1 % slower on C4
   static constexpr int kBins = 1 << kBits;
   static constexpr int kKeyBits = sizeof(Key) * 8;
   using Scan = cub::BlockScan<int, kThreads>;

@@ -128,7 +128,7 @@ def vs_estimate_async(q: torch.Tensor, k: torch.Tensor, cfg: VerticalSlash, head
     dt = _dtype_code(q)
     lib = _lib.load()
     ws_bytes = lib.spf_vs_estimate_workspace_size(code, dt, hq, hkv, n, s_len, d, cfg.last_q)
-    ws = _dev.workspace(ws_bytes, dev)
+    ws = _dev.workspace(ws_bytes, dev, stream)
     _lib.check(lib.spf_vs_estimate(code, dt, _dev.ptr(q.contiguous()), _dev.ptr(k.contiguous()), hq, hkv, s_len, d,
                                    _dev.ptr(head_ids), n, cfg.last_q, cfg.k_v, cfg.k_s, _dev.ptr(vert), _dev.ptr(sl),
                                    _dev.ptr(vsc), _dev.ptr(ssc), _dev.ptr(flags), _dev.ptr(ws), ws_bytes,
@@ -167,7 +167,7 @@ def estimate_block_sparse_gpu(q: torch.Tensor, k: torch.Tensor, cfg: BlockSparse
     n = hq if head_ids is None else int(head_ids.numel())
     lib = _lib.load()
     ws_bytes = bs_workspace_bytes(hq, hkv, s_len, d, cfg.block_size, n)
-    ws = _dev.workspace(ws_bytes, dev)
+    ws = _dev.workspace(ws_bytes, dev, stream)
     _lib.check(lib.spf_bs_estimate(_dtype_code(q), _dev.ptr(q.contiguous()), _dev.ptr(k.contiguous()), hq, hkv, s_len,
                                    d, _dev.ptr(head_ids), n, cfg.k_b, cfg.block_size, _dev.ptr(tile_offsets),
                                    _dev.ptr(tile_starts), _dev.ptr(ws), ws_bytes, _dev.stream_handle(stream)),

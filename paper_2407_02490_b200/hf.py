@@ -44,6 +44,15 @@ def _layer_cfgs(layer_idx: int, n_heads: int):
     return row
 
 
+def _is_unpadded_causal(mask: torch.Tensor) -> bool:
+    """A causal mask without padding lets the last query see every key: check that row
+    (bool masks: True = attend; additive masks: 0 = attend)."""
+    last = mask[..., -1, :]
+    if mask.dtype == torch.bool:
+        return bool(last.all())
+    return bool((last == 0).all())
+
+
 def sparse_prefill_attention_forward(module, query, key, value, attention_mask, scaling=None, dropout=0.0,
                                      **kwargs):
     """transformers AttentionInterface signature: query [B, Hq, Sq, d], key/value
@@ -54,11 +63,12 @@ def sparse_prefill_attention_forward(module, query, key, value, attention_mask, 
     sk = key.shape[2]
     scale = scaling if scaling is not None else d ** -0.5
     if sq != sk:  # decode / chunked continuation: dense, like MInference
-        out = F.scaled_dot_product_attention(query, key, value, attn_mask=None, is_causal=False, scale=scale,
-                                             enable_gqa=hq != key.shape[1]) if sq == 1 else \
-            F.scaled_dot_product_attention(query, key, value, attn_mask=attention_mask, scale=scale,
-                                           enable_gqa=hq != key.shape[1])
+        out = F.scaled_dot_product_attention(query, key, value, attn_mask=attention_mask, scale=scale,
+                                             enable_gqa=hq != key.shape[1])
         return out.transpose(1, 2).contiguous(), None
+    if attention_mask is not None and not _is_unpadded_causal(attention_mask):
+        raise ValueError("the sparse pre-fill path supports unpadded causal batches only "
+                         "(the attention mask hides keys from the last query: padding)")
     cfgs = _layer_cfgs(getattr(module, "layer_idx", 0), hq)
     bs = next((c.block_size for c in cfgs if isinstance(c, BlockSparse)), 64)
     outs = []

@@ -54,6 +54,12 @@ def _pair_list(pair_heads, hq: int, dev) -> torch.Tensor | None:
         return None
     if pair_heads.numel() > hq:
         raise ValueError("more pair heads than q-heads")
+    if pair_heads.device.type == "cpu":  # host ids: validate here (device lists are routed by the
+        ids = pair_heads.reshape(-1)    # library, which never leaves a head unwritten)
+        if int(ids.min()) < 0 or int(ids.max()) >= hq:
+            raise ValueError(f"pair head ids must lie in [0, {hq})")
+        if torch.unique(ids).numel() != ids.numel():
+            raise ValueError("pair head ids must be distinct")
     return pair_heads.to(device=dev, dtype=torch.int32).contiguous()
 
 
@@ -69,11 +75,13 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     CSR over (head, row): offsets int64 [Hq*n_rows+1], entries int32.
     Returns out [Hq, S, d] in the input dtype.  ``lse`` (optional fp32 [Hq, S])
     receives each row's natural-log sum of exp(scale * q.k) over its cells.
-    ``pair_heads`` (optional) names the heads without residual columns whose row
-    blocks rarely share tiles (Block-Sparse heads): they run the paired-box kernel
-    (include/spf.h, spf_sparse_flash_rows_ex).  Either a device int32 tensor of
-    distinct head ids (the hot path: its length is host metadata, no sync), or a bool /
-    uint8 [Hq] mask (converted here).
+    ``pair_heads`` (optional) names candidate heads for the paired-box kernel (Block-Sparse
+    heads, whose row blocks rarely share tiles); the library measures each listed head's
+    layout on the device and runs it there only when it has no residual columns and the
+    paired steps beat the union steps (include/spf.h, spf_sparse_flash_rows_ex); every other
+    head runs the union kernel.  Either a device int32 tensor of head ids (the hot path: its
+    length is host metadata, no sync), a host id list (validated: distinct, in range), or a
+    bool / uint8 [Hq] mask (converted here).
     """
     dev = _dev.require_cuda(q.device)
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
@@ -93,7 +101,7 @@ def sparse_flash_attention_gpu(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
         out = torch.empty_like(q)
     lib = _lib.load()
     ws_bytes = lib.spf_sparse_flash_workspace_size(dtype, hq, hkv, s_len, d)
-    ws = _dev.workspace(ws_bytes, dev)
+    ws = _dev.workspace(ws_bytes, dev, stream)
     ts = tile_starts if tile_starts.numel() else None
     cs = col_indices if col_indices.numel() else None
     if lse is not None and (lse.dtype != torch.float32 or lse.numel() != hq * s_len or not lse.is_contiguous()):

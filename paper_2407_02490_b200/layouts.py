@@ -29,7 +29,7 @@ def csr_offsets(counts: torch.Tensor, stream=None, want_total: bool = True):
     n = counts.numel()
     offsets = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
     ws_bytes = lib.spf_scan_workspace_size(n)
-    ws = _dev.workspace(ws_bytes, counts.device)
+    ws = _dev.workspace(ws_bytes, counts.device, stream)
     total = _i64_host() if want_total else None
     _lib.check(lib.spf_csr_offsets(_dev.ptr(counts), n, _dev.ptr(offsets), total, _dev.ptr(ws), ws_bytes,
                                    _dev.stream_handle(stream)), "spf_csr_offsets")

@@ -82,7 +82,15 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
     """Estimation + index compaction for every head of a layer (steps 1-2).
 
     ``groups`` may pass the layer's precomputed device head groups
-    (driver.PatternTable.device_groups) instead of regrouping ``head_cfgs``."""
+    (driver.PatternTable.device_groups) instead of regrouping ``head_cfgs``.  With a
+    ``stream``, every allocation, kernel and copy of the layer is ordered on it."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return _build_layer_layout(q, k, head_cfgs, block_size, stream, groups)
+    return _build_layer_layout(q, k, head_cfgs, block_size, None, groups)
+
+
+def _build_layer_layout(q, k, head_cfgs, block_size, stream, groups) -> LayerLayout:
     dev = _dev.require_cuda(q.device)
     hq, s_len, _ = q.shape
     if len(head_cfgs) != hq:
@@ -145,6 +153,9 @@ def sparse_prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, 
                              scale: float | None = None, out: torch.Tensor | None = None, stream=None,
                              return_layout: bool = False, groups=None):
     """Full layer: q [Hq, S, d], k/v [Hkv, S, d] (bf16) -> out [Hq, S, d]."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return sparse_prefill_attention(q, k, v, head_cfgs, block_size, scale, out, None, return_layout, groups)
     layout = build_layer_layout(q, k, head_cfgs, block_size, stream, groups)
     d = q.shape[-1]
     sc = 1.0 / math.sqrt(d) if scale is None else float(scale)

@@ -3,7 +3,8 @@ reference kernel contract (_core.pyx:72-192) restated in oracle/port.py and
 against the reference's own outputs stored in tests/golden.
 
 Tolerances (BASELINE.json north_star): fp32 I/O -> max-abs error <= 1e-3 x
-max(1, max|ref|) ("1e-3 relative"); bf16 I/O -> max-abs <= 2e-2.
+max|ref| ("1e-3 relative", relative to the output's own scale, however small);
+bf16 I/O -> max-abs <= 2e-2.
 """
 
 import math
@@ -22,8 +23,9 @@ BF16_TOL = 2e-2
 
 
 def rel_err(got, want):
-    return float(np.max(np.abs(got.astype(np.float64) - want.astype(np.float64)))) / max(
-        1.0, float(np.max(np.abs(want))))
+    scale = float(np.max(np.abs(want)))
+    err = float(np.max(np.abs(got.astype(np.float64) - want.astype(np.float64))))
+    return err / scale if scale > 0 else err
 
 
 def max_abs(got, want):
@@ -203,6 +205,82 @@ def test_pair_heads_validation(K):
         K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.float32, device=dev))
     out = K.sparse_flash_attention_gpu(*args, pair_heads=torch.zeros(2, dtype=torch.uint8, device=dev))
     assert out.abs().max().item() == 0  # no coverage -> zero rows; empty list = union kernel only
+    for bad in ([0, 0], [0, 5], [-1]):  # host id lists are validated: distinct, in range
+        with pytest.raises(ValueError):
+            K.sparse_flash_attention_gpu(*args, pair_heads=torch.tensor(bad, dtype=torch.int32))
+
+
+def _bs_case(hq, hkv, s, d, kb, seed, b=64):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    q = bf16_round(rng.standard_normal((hq, s, d)).astype(np.float32))
+    k = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    v = bf16_round(rng.standard_normal((hkv, s, d)).astype(np.float32))
+    n = (s + b - 1) // b
+    tiles_all = []
+    for _h in range(hq):
+        for r in range(n):
+            m = min(kb, r + 1)
+            blocks = sorted(set([r] + rng.choice(r + 1, size=m, replace=False).tolist()))[-m:]
+            if r not in blocks:
+                blocks[-1] = r
+            tiles_all.append(sorted(x * b for x in blocks))
+    return q, k, v, n, tiles_all, rng
+
+
+def test_pair_device_list_duplicates_never_drop_a_head(K):
+    """a device list [0, 0] (or with an out-of-range id) must not leave head 1
+    unwritten -- the union kernel runs every head the paired-box kernel does not."""
+    hq, hkv, s, d, b = 2, 1, 2048 + 77, 64, 64
+    q, k, v, n, tiles_all, _ = _bs_case(hq, hkv, s, d, 6, 5)
+    ts, to = port.flatten(tiles_all)
+    co = np.zeros(hq * n + 1, np.int64)
+    dev = torch.device("cuda")
+    args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+            torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+            torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+            torch.zeros(1, dtype=torch.int32, device=dev), torch.from_numpy(co).to(dev))
+    for ids in ([0, 0], [0, 5], [7, -3]):
+        out = torch.full((hq, s, d), float("nan"), dtype=torch.bfloat16, device=dev)
+        got = K.sparse_flash_attention_gpu(*args, out=out,
+                                           pair_heads=torch.tensor(ids, dtype=torch.int32, device=dev))
+        got = got.float().cpu().numpy()
+        for h in range(hq):
+            tt, tto = port.flatten(tiles_all[h * n:(h + 1) * n])
+            want = port.sparse_flash_rows(q[h], k[0], v[0], 1 / math.sqrt(d), b, tt, tto,
+                                          np.zeros(0, np.int64), np.zeros(n + 1, np.int64))
+            assert np.isfinite(got[h]).all(), (ids, h)
+            assert max_abs(got[h], want) < BF16_TOL, (ids, h)
+
+
+def test_listed_head_with_columns_runs_union_kernel(K):
+    """the paired-box kernel has no column-chip path; a listed head (here: every
+    head listed, so no unlisted head forces a union launch) that has residual columns must
+    still get them -- it is routed to the union kernel."""
+    hq, hkv, s, d, b = 2, 1, 4096 + 13, 64, 64
+    q, k, v, n, tiles_all, rng = _bs_case(hq, hkv, s, d, 5, 9)
+    cols_all = []
+    for h in range(hq):
+        for r in range(n):
+            covered = set()
+            for t in tiles_all[h * n + r]:
+                covered.update(range(t, min(t + b, s)))
+            cand = [j for j in range(0, min(s, r * b + b)) if j not in covered]
+            pick = sorted(rng.choice(cand, size=min(len(cand), 70 if h == 1 else 0), replace=False).tolist())
+            cols_all.append(pick)
+    ts, to = port.flatten(tiles_all)
+    cs, co = port.flatten(cols_all)
+    dev = torch.device("cuda")
+    args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+            torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+            torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+            torch.from_numpy(cs.astype(np.int32)).to(dev), torch.from_numpy(co).to(dev))
+    got = K.sparse_flash_attention_gpu(*args, pair_heads=torch.arange(hq, dtype=torch.int32, device=dev))
+    got = got.float().cpu().numpy()
+    for h in range(hq):
+        tt, tto = port.flatten(tiles_all[h * n:(h + 1) * n])
+        cc, cco = port.flatten(cols_all[h * n:(h + 1) * n])
+        want = port.sparse_flash_rows(q[h], k[0], v[0], 1 / math.sqrt(d), b, tt, tto, cc, cco)
+        assert max_abs(got[h], want) < BF16_TOL, (h, max_abs(got[h], want))
 
 
 def test_mixed_layer_routes_block_sparse_heads_by_overlap(K):

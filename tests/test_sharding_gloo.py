@@ -132,3 +132,23 @@ def test_two_rank_gloo_sharded_layer(world, plan):
     assert result["shape"] == (6, 96, 16)
     assert result["max_err"] == 0.0  # same CPU computation, reassembled in head order
     assert result["t"] == float(world)  # max over ranks
+
+
+def test_bench_spawns_world_size_ranks():
+    """`python bench.py --gpus 2` without torchrun env must launch 2 ranks itself (torchrun
+    re-exec, 127.0.0.1 rendezvous), take the max over ranks and print ONE JSON line with
+    n_gpus 2 from rank 0 (--dry-run: the same launch and reduction over gloo, no GPU)."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=repo)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, res.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["value"] == 2.0  # max over the ranks' 1.0 and 2.0
+    assert rec["rank0_q_heads"] == list(range(16))

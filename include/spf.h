@@ -117,13 +117,21 @@ int spf_argtopk(const double* values, int64_t n, int k, int32_t* out, void* work
  * index 0 force-included (estimator.py:59-79).
  *   mode SPF_VS_EXACT : scores in fp64 from the bf16/fp32 inputs, sums in
  *                       fp64 in the reference's order (any shape);
- *   mode SPF_VS_FAST  : scores on the tensor cores (tcgen05, fp32 accumulate)
- *                       for bf16 inputs with head_dim 64/128 and last_q 64
- *                       (other shapes run the exact path).  The top-k of each
- *                       head is certified against this path's error model;
- *                       uncertain_out[i] = 1 marks a head whose selection is
- *                       too close to call, which the caller re-runs with
- *                       SPF_VS_EXACT to get the reference's set.
+ *   mode SPF_VS_FAST  : production path.  Scores on the tensor cores (tcgen05,
+ *                       fp32 accumulate) for bf16 inputs with head_dim 64/128
+ *                       and last_q 64 (other shapes run the exact path).  A
+ *                       rigorous bound on the score error (gamma_d * sum_c
+ *                       |q_c| max_j |k_jc|, estimate_vs_tc.cu) gives every
+ *                       score-vector entry an interval; a head whose top-k
+ *                       boundary is not separated by those intervals -- or
+ *                       whose bound is too loose to try -- is re-estimated on
+ *                       the fp64 path inside this call (same stream, no host
+ *                       sync), skipping only keys whose probabilities provably
+ *                       round to 0 in fp32.  The sets equal SPF_VS_EXACT's.
+ *                       uncertain_out[i] = 1 marks the heads that were re-run.
+ *   mode SPF_VS_FAST_UNCERTIFIED : test hook -- the tensor-core path alone
+ *                       (no re-estimation; uncertain_out still reports the
+ *                       heads the certification rejects).  Not exact.
  *   vertical_out : [n_heads][min(k_v, S)] int32, ascending
  *   slash_out    : [n_heads][min(k_s, S)] int32, descending
  *   vscore_out / sscore_out : optional [n_heads][seq_len] fp64 score vectors
@@ -132,6 +140,7 @@ int spf_argtopk(const double* values, int64_t n, int k, int32_t* out, void* work
  * ------------------------------------------------------------------------- */
 #define SPF_VS_EXACT 0
 #define SPF_VS_FAST 1
+#define SPF_VS_FAST_UNCERTIFIED 2
 size_t spf_vs_estimate_workspace_size(int mode, int dtype, int n_q_heads, int n_kv_heads, int n_heads, int seq_len,
                                       int head_dim, int last_q);
 int spf_vs_estimate(int mode, int dtype, const void* q, const void* k, int n_q_heads, int n_kv_heads, int seq_len,

@@ -17,6 +17,7 @@ SPF_DTYPE_BF16 = 0
 SPF_DTYPE_F32 = 1
 SPF_VS_EXACT = 0
 SPF_VS_FAST = 1
+SPF_VS_FAST_UNCERTIFIED = 2  # test hook: tensor-core path without re-estimation (not exact)
 
 _c_int = ctypes.c_int
 _c_float = ctypes.c_float

@@ -21,6 +21,10 @@
 
 namespace spf {
 
+// certification: absolute uncertainty of a vector entry from flushed exponentials
+// (<= 64 probabilities below 2^-126 each, set to 0 by ex2.approx.ftz)
+constexpr double kFlushAbs = 64.0 * 0x1p-126;
+
 template <int kThreads, int kCl>
 struct ClusterTopK {
   static constexpr int kBits = 11;
@@ -236,12 +240,18 @@ struct ClusterTopK {
         eqs += sm.eq[r];
       }
       const double T = __longlong_as_double((long long)((thr >> 63) ? (thr & ~(1ull << 63)) : ~thr));
-      const double margin = (double)(*tau) * T;
+      // every entry x of the vector is within x * eta + kFlushAbs of its exact value
+      // (eta: vs_tc_combine_kernel; kFlushAbs: <= 64 terms flushed to zero below 2^-126
+      // by ex2.approx.ftz), so an order is certain when the intervals do not overlap
+      const double eta = (double)(*tau);
       const double v0 = vals[0];
+      auto apart = [&](double big, double small) {  // exact big > exact small, guaranteed
+        return big * (1.0 - eta) - kFlushAbs > small * (1.0 + eta) + kFlushAbs;
+      };
       bool f = eqs > krem;                                   // the k-th value ties with an unselected one
-      f |= !(T - lo > margin);                               // k-th vs (k+1)-th
-      f |= !(fabs(v0 - T) > margin);                         // index 0 sits on the boundary
-      if (v0 < T) f |= krem >= 2 || !(hi - T > margin);      // forced 0 drops the k-th: k-th vs (k-1)-th
+      f |= !apart(T, lo);                                    // k-th vs (k+1)-th
+      f |= !(v0 > T ? apart(v0, T) : apart(T, v0));          // index 0 sits on the boundary
+      if (v0 < T) f |= krem >= 2 || !apart(hi, T);           // forced 0 drops the k-th: k-th vs (k-1)-th
       if (f) atomicOr(flag, 1);
     }
     int eq_glob = 0;

@@ -345,7 +345,7 @@ extern "C" {
 
 size_t spf_vs_estimate_workspace_size(int mode, int dtype, int n_q_heads, int n_kv_heads, int n_heads, int seq_len,
                                       int head_dim, int last_q) {
-  if (mode == SPF_VS_FAST && vs_fast_supported(dtype, head_dim, seq_len, last_q))
+  if (mode != SPF_VS_EXACT && vs_fast_supported(dtype, head_dim, seq_len, last_q))
     return vs_fast_workspace_size(n_q_heads, n_kv_heads, n_heads, seq_len);
   return vs_exact_workspace_size(n_heads, seq_len, last_q);
 }
@@ -354,7 +354,8 @@ int spf_vs_estimate(int mode, int dtype, const void* q, const void* k, int n_q_h
                     int head_dim, const int32_t* head_ids, int n_heads, int last_q, int k_v, int k_s,
                     int32_t* vertical_out, int32_t* slash_out, double* vscore_out, double* sscore_out,
                     int32_t* uncertain_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (mode != SPF_VS_EXACT && mode != SPF_VS_FAST) return set_error(SPF_ERR_INVALID, "unknown estimation mode %d", mode);
+  if (mode != SPF_VS_EXACT && mode != SPF_VS_FAST && mode != SPF_VS_FAST_UNCERTIFIED)
+    return set_error(SPF_ERR_INVALID, "unknown estimation mode %d", mode);
   if (dtype != SPF_DTYPE_BF16 && dtype != SPF_DTYPE_F32) return set_error(SPF_ERR_INVALID, "unknown dtype %d", dtype);
   if (last_q < 1 || k_v < 1 || k_s < 1) return set_error(SPF_ERR_INVALID, "Vertical-Slash counts must be >= 1");
   if (last_q > seq_len) return set_error(SPF_ERR_INVALID, "last_q=%d exceeds seq_len=%d", last_q, seq_len);
@@ -368,15 +369,16 @@ int spf_vs_estimate(int mode, int dtype, const void* q, const void* k, int n_q_h
   const int kv = min(k_v, seq_len), ks = min(k_s, seq_len);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  if (mode == SPF_VS_FAST && vs_fast_supported(dtype, head_dim, seq_len, last_q))
+  if (mode != SPF_VS_EXACT && vs_fast_supported(dtype, head_dim, seq_len, last_q))
     return vs_estimate_fast(q, k, n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, kv, ks, vertical_out,
-                            slash_out, vscore_out, sscore_out, uncertain_out, ws, st);
+                            slash_out, vscore_out, sscore_out, uncertain_out, mode == SPF_VS_FAST_UNCERTIFIED, ws,
+                            st);
   if (uncertain_out != nullptr) {
     int rc = check_cuda(cudaMemsetAsync(uncertain_out, 0, (size_t)n_heads * sizeof(int32_t), st), "memset flags");
     if (rc) return rc;
   }
   return vs_exact_run(dtype, q, k, n_q_heads, n_kv_heads, seq_len, head_dim, head_ids, n_heads, last_q, kv, ks,
-                      vertical_out, slash_out, vscore_out, sscore_out, nullptr, nullptr, nullptr, ws, st);
+                      vertical_out, slash_out, vscore_out, sscore_out, nullptr, nullptr, nullptr, nullptr, ws, st);
 }
 
 size_t spf_bs_estimate_workspace_size(int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int block_size) {

@@ -21,8 +21,10 @@
 // Fallback mode: `gate` restricts the work to flagged heads (device-side, no
 // host sync) and `tile_max` (per row and 128-key tile, from the tensor-core
 // pass) lets an item be skipped when every score in it is below the row max
-// by more than 152 in log2 units: such p are < 2^-150 and round to exactly 0
-// in fp32 (l_i >= 1), i.e. the skip is exact, not an approximation.
+// by more than 151 + row_marg in log2 units: row_marg is twice the rigorous bound
+// on the tensor-core score error (estimate_vs_tc.cu, vs_tc_combine_kernel), so
+// the exact scores are > 150 below the exact row max, such p are < 2^-150 and
+// round to exactly 0 in fp32 (l_i >= 1): the skip is exact, not an approximation.
 #include <algorithm>
 #include <cuda_bf16.h>
 
@@ -46,6 +48,7 @@ struct ExArgs {
   const int32_t* gate;     // nullable
   const float* tile_max;   // nullable: [n_heads][64][ceil(S/128)] raw fp32 scores
   const float* row_mc;     // [n_heads][64]: fp32(max raw score * c)
+  const float* row_marg;   // [n_heads][64]: 2 x score-error bound of the tensor-core scores (log2 units)
   float c;                 // scale * log2(e)
   double scale;
   double2* stats;          // [n_heads][L][n_kblk]
@@ -131,7 +134,7 @@ __device__ void score_tile(ExSmem& sm, const T* qh, const T* kh, int r0, int n_r
   }
 }
 
-// Is any score of item (h, kb) within 152 (log2 units) of its row max?  Exact-skip test.
+// Is any score of item (h, kb) within 151 + margin (log2 units) of its row max?  Exact-skip test.
 __device__ bool item_significant(const ExArgs& a, int h, int k0) {
   if (a.tile_max == nullptr) return true;
   const int n_t = (a.S + 127) / 128;
@@ -140,7 +143,8 @@ __device__ bool item_significant(const ExArgs& a, int h, int k0) {
   if (threadIdx.x < 64) {
     const float tm = a.tile_max[((int64_t)h * 64 + threadIdx.x) * n_t + t];
     const float mc = a.row_mc[(int64_t)h * 64 + threadIdx.x];
-    sig = !(tm * a.c - mc < -152.f);  // NaN-safe: anything unexpected counts as significant
+    const float mg = a.row_marg[(int64_t)h * 64 + threadIdx.x];
+    sig = !(tm * a.c - mc < -151.f - mg);  // NaN-safe: anything unexpected counts as significant
   }
   return __syncthreads_or(sig) != 0;
 }
@@ -160,7 +164,8 @@ __global__ void vs_exact_prep_kernel(const ExArgs a) {
   for (int i = lane; i < 64; i += 32) {
     const float tm = a.tile_max[((int64_t)h * 64 + i) * n_t + t];
     const float mc = a.row_mc[(int64_t)h * 64 + i];
-    sig |= !(tm * a.c - mc < -152.f);
+    const float mg = a.row_marg[(int64_t)h * 64 + i];
+    sig |= !(tm * a.c - mc < -151.f - mg);
   }
   sig = __any_sync(0xffffffffu, sig);
   for (int o = k0 + lane; o < min(k0 + a.KB, S); o += 32) a.sscore[(int64_t)h * S + o] = 0.0;
@@ -406,7 +411,8 @@ size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q) {
 
 int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
                  int n_heads, int L, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                 const int32_t* gate, const float* tile_max, const float* row_mc, void* workspace, cudaStream_t st) {
+                 const int32_t* gate, const float* tile_max, const float* row_mc, const float* row_marg,
+                 void* workspace, cudaStream_t st) {
   if (L > kMaxL) return set_error(SPF_ERR_INVALID, "last_q=%d exceeds the supported %d", L, kMaxL);
   ExArgs a{};
   a.S = S;
@@ -420,6 +426,7 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
   a.gate = gate;
   a.tile_max = (L == 64 && a.KB == 64) ? tile_max : nullptr;
   a.row_mc = row_mc;
+  a.row_marg = row_marg;
   a.scale = 1.0 / sqrt((double)d);
   a.c = (float)(a.scale * 1.4426950408889634);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);

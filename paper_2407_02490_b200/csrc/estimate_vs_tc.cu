@@ -41,8 +41,9 @@ constexpr int kTailRows = 64;     // last_q supported by this path
 constexpr int kMaxMembers = 4;    // q-heads per group
 constexpr int kKeys = 128;        // keys per tile (UMMA M of pass 2, N of pass 1)
 constexpr int kStages = 4;        // K tile stages
-constexpr int kThreads = 320;     // 10 warps
+constexpr int kThreads = 352;     // 11 warps
 constexpr int kEpiThreads = 256;  // warps 2..9
+constexpr int kStatWarp = 10;     // pass 1: per-tile K statistics for the score error bound
 constexpr int kGroupRows = kMaxMembers * kTailRows;
 
 struct TcArgs {
@@ -53,13 +54,20 @@ struct TcArgs {
   float* st_m;       // [groups][chunks][256]  mc = fp32(row max * c)
   double* st_l;      // [groups][chunks][256]
   float* st_amax;    // [groups][chunks][256]
+  // pass 1 out: max_j |k_jc| per group and dimension (bf16 bits in the low half; zeroed first)
+  uint32_t* kabs;             // [groups][kD]
+  // combine out
+  float* row_marg;            // [n_heads][64]: 2 * score-error bound in log2 units (fp64 path's skip margin)
+  int32_t* hopeless;          // [n_heads]: 1 = the bound is too loose to certify: straight to the fp64 path
+  int32_t* flags;             // [n_heads]: 1 = the fp64 path re-estimates the head
+  int uncertified;            // test hook: no hopeless short-cut, no re-estimation
   // combine out / pass 2 in
   float* row_m;      // [groups][256]  mc of the global row max
   float* row_il;     // [groups][256]
   // pass 2 out
   double* vscore;    // [n_heads][S]
   double* sscore;    // [n_heads][S]  (zeroed before pass 2)
-  float* tau;        // [n_heads] relative certification threshold
+  float* tau;        // [n_heads] eta: bound on the relative error of every score-vector entry
   // for the exact fallback's tile skipping
   float* tile_max;   // [n_heads][64][n_tiles] raw row max per 128-key tile
   float* row_mc;     // [n_heads][64] mc per slot
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&ctrl->q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&ctrl->k_full[s], 1);
-      mbar_init(&ctrl->k_empty[s], 1);
+      mbar_init(&ctrl->k_empty[s], kPass == 1 ? 2 : 1);  // pass 1: MMA commit + K-statistics warp
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctrl->acc_full[b], 1);
@@ -154,6 +162,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   const int nh = ctrl->nh;
   if (nh == 0 || chunk >= a.n_tiles) return;  // CTA-uniform, before TMEM allocation
+  if (kPass == 2) {  // every member goes to the fp64 path anyway: no pass 2 for this group
+    bool all_hopeless = true;
+    for (int mm = 0; mm < nh; ++mm) all_hopeless = all_hopeless && a.hopeless[ctrl->slot[mm]] != 0;
+    if (all_hopeless) return;
+  }
   if (kPass == 2) {
     // row stats per member pair and tail row: {-mc(2p), -mc(2p+1), 1/l(2p), 1/l(2p+1)}
     float4* rs = reinterpret_cast<float4*>(smem + L::kOffRow);
@@ -269,6 +282,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
+  } else if (warp == kStatWarp) {
+    // ======================= K statistics (pass 1 only) =========================
+    // max_j |k_jc| per dimension c over the group's keys: the input of the bound on the
+    // tensor-core score error (vs_tc_combine_kernel).  Lane l owns the 8 dims of logical
+    // 16-byte chunk (l & 15) and the keys of half (l >> 4) of every staged SW128 tile
+    // (each 128-byte row holds 64 dims of one key, chunks permuted by row & 7).
+    if (kPass == 1) {
+      const int cc = lane & 15, at = cc >> 3, c = cc & 7, kh = lane >> 4;
+      uint32_t amx[4] = {0u, 0u, 0u, 0u};  // |k| maxima of the lane's 8 dims, bf16x2
+      for (int t = 0; t < n_tiles_cta; ++t) {
+        const int st = t % kStages;
+        mbar_wait(&ctrl->k_full[st], (t / kStages) & 1);
+        const uint8_t* kst = smem + L::kOffK + st * L::kStageBytes + at * L::kKAtom;
+        // keys past S are TMA zero fill: they cannot raise a maximum
+#pragma unroll 8
+        for (int r = kh * 64; r < kh * 64 + 64; ++r) {
+          const uint4 x = *reinterpret_cast<const uint4*>(kst + r * 128 + ((c ^ (r & 7)) << 4));
+          // bf16 magnitudes order like their bit patterns: per-half unsigned max
+          amx[0] = __vmaxu2(amx[0], x.x & 0x7fff7fffu);
+          amx[1] = __vmaxu2(amx[1], x.y & 0x7fff7fffu);
+          amx[2] = __vmaxu2(amx[2], x.z & 0x7fff7fffu);
+          amx[3] = __vmaxu2(amx[3], x.w & 0x7fff7fffu);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctrl->k_empty[st]);  // K consumed: the stage may be refilled
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) amx[w] = __vmaxu2(amx[w], __shfl_xor_sync(0xffffffffu, amx[w], 16));
+      if (kh == 0 && n_tiles_cta > 0) {
+        uint32_t* dst = a.kabs + (int64_t)gy * kD + at * 64 + c * 8;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          atomicMax(dst + 2 * w, amx[w] & 0xffffu);
+          atomicMax(dst + 2 * w + 1, amx[w] >> 16);
+        }
+      }
+    }
   } else {
     // =============================== epilogue warps =============================
     // Exponents are formed as y = s*c - mc with one FFMA, c = scale*log2(e) and
@@ -459,18 +509,50 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Per-row combine of the chunk partials (fp64), per-head certification threshold.
-__global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs a) {
+// Error model of the tensor-core scores (no tcgen05 accumulation spec is published, so the
+// bound assumes the weakest behaviour consistent with fp32 accumulation): bf16 x bf16
+// products are exact; each K=16 MMA step adds its 16 products to the accumulator after
+// aligning all 17 addends to the largest with at least 24 kept bits (truncation), then
+// rounds (or truncates) to fp32.  One step errs by <= 17 * 2^-23 * max addend + 2^-23 * |sum|
+// <= 18 * 2^-23 * (sum of |products| so far), so over d/16 steps
+//     |fl(q.k) - q.k| <= gamma * sum_c |q_c| |k_c|,   gamma = (d/16) * 18 * 2^-23,
+// and sum_c |q_c||k_c| <= sum_c |q_c| * max_j |k_jc| (the per-dimension maxima of pass 1).
+// The bound is rigorous under that model, whatever the cancellation in q.k (it scales with
+// sum |q_c k_c|, not with |q.k|), and it is the same for pass 2's transposed product.
+template <int kD>
+__device__ __forceinline__ double score_gamma() { return (kD / 16) * 18.0 * 0x1p-23; }
+
+// Per-row combine of the chunk partials (fp64); per row the score-error bound E_i and the
+// fp64 path's skip margin; per head the certification bound eta and the hopeless flag.
+//
+// eta bounds the relative error of every vertical / slash entry of the fast path against
+// the reference's fp64 values (estimator.py:100-110 with tensor.py:78's fp32 rounding):
+//   p = exp(s_ij) / sum_k exp(s_ik): numerator and normaliser each off by <= e^(c' E_i) with
+//   c' = scale (nats per raw unit)                                -> expm1(2 scale E_max)
+//   the fp32 constant c_hi = fl(scale log2 e) scales every exponent: |x| c 2^-24 per side
+//                                                                  -> 2 ln2 c amax 2^-24
+//   ex2.approx (2^-21), fp32 partial row sums (2^-19), 1/l and p roundings, the
+//   reference's own fp32 rounding of p, fp32 partial column / diagonal sums (2^-18)
+//                                                                  -> 2^-16 (with margin)
+// Values flushed to zero by ex2.approx.ftz (true p < 2^-126) are the absolute term of the
+// certification (cluster_topk.cuh).
+constexpr double kHopelessEta = 0x1p-12;  // larger: no top-k boundary of a long sequence is that wide
+template <int kD>
+__global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs a, const __nv_bfloat16* __restrict__ q) {
   __shared__ int slot[kMaxMembers], head[kMaxMembers], nh_s;
   __shared__ float amax_s[kGroupRows];
+  __shared__ float err_s[kGroupRows];
+  __shared__ float kabs_s[kD];
   const int gy = blockIdx.x;
   if (threadIdx.x == 0) nh_s = group_members(a, gy, slot, head);
+  for (int c = threadIdx.x; c < kD; c += blockDim.x)
+    kabs_s[c] = __uint_as_float(a.kabs[(int64_t)gy * kD + c] << 16);
   __syncthreads();
   const int nh = nh_s;
   const int r = threadIdx.x;
   const int mm = r / kTailRows;
   const double c64 = (double)a.c_hi + (double)a.c_lo;
-  float amax = 0.f;
+  float amax = 0.f, err = 0.f;
   if (mm < nh) {
     float m = -INFINITY;
     for (int c = 0; c < a.n_chunks; ++c) {
@@ -486,17 +568,34 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
     }
     a.row_m[(int64_t)gy * kGroupRows + r] = m;
     a.row_il[(int64_t)gy * kGroupRows + r] = (float)(1.0 / l);
-    a.row_mc[(int64_t)slot[mm] * kTailRows + (r % kTailRows)] = m;
+    const int i = r % kTailRows;
+    a.row_mc[(int64_t)slot[mm] * kTailRows + i] = m;
+    // E_i = gamma * sum_c |q_ic| max_j |k_jc| (fp64: exact products of bf16 values, tiny sum error)
+    const __nv_bfloat16* qr = q + ((int64_t)head[mm] * a.S + (a.S - kTailRows + i)) * kD;
+    double sabs = 0.0;
+    for (int c = 0; c < kD; ++c) sabs += fabs((double)__bfloat162float(qr[c])) * (double)kabs_s[c];
+    const double e_i = score_gamma<kD>() * sabs * (1.0 + 0x1p-40);
+    err = (float)(e_i * (1.0 + 0x1p-20));
+    // fp64 path: an item is skipped when its tensor-core scores sit > 151 + marg (log2 units)
+    // below the row max; the true scores can be E_i higher and the true max E_i lower
+    a.row_marg[(int64_t)slot[mm] * kTailRows + i] = (float)(2.0 * e_i * c64 * (1.0 + 0x1p-20));
   }
   amax_s[r] = amax;
+  err_s[r] = err;
   __syncthreads();
   if (r < nh) {
-    float mx = 0.f;
-    for (int i = 0; i < kTailRows; ++i) mx = fmaxf(mx, amax_s[r * kTailRows + i]);
-    // error model of the fp32 path: a few fp32 ulps of the largest |score| (natural-log units),
-    // relative to the probabilities; 2^-20 leaves a ~10x margin over the measured error.
-    const double smax = (double)mx * c64 * 0.6931471805599453;
-    a.tau[slot[r]] = (float)(ldexp(1.0, -20) * (1.0 + smax));
+    float mx = 0.f, emax = 0.f;
+    for (int i = 0; i < kTailRows; ++i) {
+      mx = fmaxf(mx, amax_s[r * kTailRows + i]);
+      emax = fmaxf(emax, err_s[r * kTailRows + i]);
+    }
+    const double scale = c64 * 0.6931471805599453;  // nats per raw score unit
+    const double eta = expm1(2.0 * scale * (double)emax) + 2.0 * 0.6931471805599453 * c64 * (double)mx * 0x1p-24 +
+                       0x1p-16;
+    a.tau[slot[r]] = (float)(eta * (1.0 + 0x1p-20));
+    const int hopeless = (eta > kHopelessEta && !a.uncertified) ? 1 : 0;
+    a.hopeless[slot[r]] = hopeless;
+    if (hopeless) a.flags[slot[r]] = 1;  // straight to the fp64 path
   }
 }
 
@@ -545,11 +644,13 @@ constexpr int kTopkCl = 8;
 
 __global__ void __cluster_dims__(kTopkCl, 1, 1) __launch_bounds__(kTopkThreads)
     vs_topk_certify_kernel(const double* __restrict__ vscore, const double* __restrict__ sscore, int S, int k_v,
-                           int k_s, const float* __restrict__ tau, int32_t* __restrict__ vert_out,
-                           int32_t* __restrict__ slash_out, int32_t* __restrict__ uncertain) {
+                           int k_s, const float* __restrict__ tau, const int32_t* __restrict__ hopeless,
+                           int32_t* __restrict__ vert_out, int32_t* __restrict__ slash_out,
+                           int32_t* __restrict__ uncertain) {
   using TK = ClusterTopK<kTopkThreads, kTopkCl>;
   __shared__ typename TK::Storage sm;
   const int hi = blockIdx.y;
+  if (hopeless[hi]) return;  // written before this launch: cluster-uniform
   if (blockIdx.z == 0)
     TK::run(sm, vscore + (int64_t)hi * S, S, k_v, false, vert_out + (int64_t)hi * k_v, tau + hi, uncertain + hi);
   else
@@ -559,7 +660,7 @@ __global__ void __cluster_dims__(kTopkCl, 1, 1) __launch_bounds__(kTopkThreads)
 template <int kD>
 int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv, int S, const int32_t* head_ids,
                  int n_heads, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                 int32_t* uncertain, uint8_t* ws, cudaStream_t st) {
+                 int32_t* uncertain, bool uncertified, uint8_t* ws, cudaStream_t st) {
   using L = TcLayout<kD>;
   TcArgs a{};
   a.S = S;
@@ -589,6 +690,9 @@ int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv
   a.row_m = reinterpret_cast<float*>(take((size_t)n_groups * kGroupRows * 4));
   a.row_il = reinterpret_cast<float*>(take((size_t)n_groups * kGroupRows * 4));
   a.tau = reinterpret_cast<float*>(take((size_t)n_heads * 4));
+  a.kabs = reinterpret_cast<uint32_t*>(take((size_t)n_groups * kD * 4));
+  a.row_marg = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * 4));
+  a.hopeless = reinterpret_cast<int32_t*>(take((size_t)n_heads * 4));
   a.vscore = vscore ? vscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   a.tile_max = reinterpret_cast<float*>(take((size_t)n_heads * kTailRows * a.n_tiles * 4));
@@ -615,21 +719,26 @@ int vs_fast_impl(const __nv_bfloat16* q, const __nv_bfloat16* k, int Hq, int Hkv
     return rc;
   int32_t* flags = uncertain ? uncertain : flags_ws;
   if (!uncertain && (rc = check_cuda(cudaMemsetAsync(flags, 0, (size_t)n_heads * 4, st), "memset flags"))) return rc;
+  if ((rc = check_cuda(cudaMemsetAsync(a.kabs, 0, (size_t)n_groups * kD * 4, st), "memset kabs"))) return rc;
+  a.flags = flags;
+  a.uncertified = uncertified ? 1 : 0;
   const dim3 grid((unsigned)a.n_chunks, (unsigned)n_groups);
   note_launches(5);  // pass 1, combine, liveness, pass 2, top-k
   vs_tc_kernel<kD, 1><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
   if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 1"))) return rc;
-  vs_tc_combine_kernel<<<n_groups, kGroupRows, 0, st>>>(a);
+  vs_tc_combine_kernel<kD><<<n_groups, kGroupRows, 0, st>>>(a, q);
   vs_tc_live_kernel<<<dim3((unsigned)((a.n_tiles + 31) / 32), (unsigned)n_groups), 256, 0, st>>>(a);
   vs_tc_kernel<kD, 2><<<grid, kThreads, L::kSmem, st>>>(tq, tk, a);
   if ((rc = check_cuda(cudaGetLastError(), "vs_tc pass 2"))) return rc;
   vs_topk_certify_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
-                                                                                        k_s, a.tau, vout, sout, flags);
+                                                                                        k_s, a.tau, a.hopeless, vout, sout,
+                                                                                        flags);
   if ((rc = check_cuda(cudaGetLastError(), "vs_tc top-k"))) return rc;
+  if (uncertified) return SPF_OK;
   // uncertified heads: fp64 re-estimation in the same stream (no host sync), skipping the
   // tiles whose probabilities round to exactly 0
   return vs_exact_run(SPF_DTYPE_BF16, q, k, Hq, Hkv, S, kD, head_ids, n_heads, kTailRows, k_v, k_s, vout, sout,
-                      a.vscore, a.sscore, flags, a.tile_max, a.row_mc, ws, st);
+                      a.vscore, a.sscore, flags, a.tile_max, a.row_mc, a.row_marg, ws, st);
 }
 
 }  // namespace
@@ -647,6 +756,7 @@ size_t vs_fast_workspace_size(int n_q_heads, int n_kv_heads, int n_heads, int se
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t part = n_groups * n_chunks * kGroupRows;
   return al(part * 4) + al(part * 8) + al(part * 4) + 2 * al(n_groups * kGroupRows * 4) + al(n_heads * 4) +
+         al(n_groups * 128 * 4) + al((size_t)n_heads * kTailRows * 4) + al(n_heads * 4) +
          2 * al((size_t)n_heads * seq_len * 8) + al((size_t)n_heads * kTailRows * n_tiles * 4) +
          al((size_t)n_heads * kTailRows * 4) + al(n_groups * n_tiles) + al(n_heads * 4) +
          vs_exact_workspace_size(n_heads, seq_len, kTailRows);
@@ -654,15 +764,15 @@ size_t vs_fast_workspace_size(int n_q_heads, int n_kv_heads, int n_heads, int se
 
 int vs_estimate_fast(const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
                      int n_heads, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                     int32_t* uncertain, void* workspace, cudaStream_t st) {
+                     int32_t* uncertain, bool uncertified, void* workspace, cudaStream_t st) {
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   const auto* qb = reinterpret_cast<const __nv_bfloat16*>(q);
   const auto* kb = reinterpret_cast<const __nv_bfloat16*>(k);
   if (d == 128)
     return vs_fast_impl<128>(qb, kb, Hq, Hkv, S, head_ids, n_heads, k_v, k_s, vout, sout, vscore, sscore, uncertain,
-                             ws, st);
-  return vs_fast_impl<64>(qb, kb, Hq, Hkv, S, head_ids, n_heads, k_v, k_s, vout, sout, vscore, sscore, uncertain, ws,
-                          st);
+                             uncertified, ws, st);
+  return vs_fast_impl<64>(qb, kb, Hq, Hkv, S, head_ids, n_heads, k_v, k_s, vout, sout, vscore, sscore, uncertain,
+                          uncertified, ws, st);
 }
 
 }  // namespace spf

@@ -62,17 +62,19 @@ int launch_sparse_attn_pairs(const AttnArgs& a, cudaStream_t stream);
 int launch_pair_stats(const AttnArgs& a, unsigned long long* stats, cudaStream_t stream);
 
 // fp64 Vertical-Slash estimation (estimate_vs_exact.cu): all heads (gate == nullptr) or the
-// flagged ones; tile_max / row_mc (from the tensor-core pass, last_q 64) enable exact tile skipping.
+// flagged ones; tile_max / row_mc / row_marg (from the tensor-core pass, last_q 64: its scores,
+// row maxima and per-row score-error margins) enable exact item skipping.
 size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q);
 int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
                  int n_heads, int L, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                 const int32_t* gate, const float* tile_max, const float* row_mc, void* workspace, cudaStream_t st);
+                 const int32_t* gate, const float* tile_max, const float* row_mc, const float* row_marg,
+                 void* workspace, cudaStream_t st);
 
 // Tensor-core Vertical-Slash estimation (estimate_vs_tc.cu), mode SPF_VS_FAST.
 bool vs_fast_supported(int dtype, int head_dim, int seq_len, int last_q);
 size_t vs_fast_workspace_size(int n_q_heads, int n_kv_heads, int n_heads, int seq_len);
 int vs_estimate_fast(const void* q, const void* k, int Hq, int Hkv, int S, int d, const int32_t* head_ids,
                      int n_heads, int k_v, int k_s, int32_t* vout, int32_t* sout, double* vscore, double* sscore,
-                     int32_t* uncertain, void* workspace, cudaStream_t st);
+                     int32_t* uncertain, bool uncertified, void* workspace, cudaStream_t st);
 
 }  // namespace spf

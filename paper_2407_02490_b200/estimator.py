@@ -124,7 +124,10 @@ def vs_estimate_async(q: torch.Tensor, k: torch.Tensor, cfg: VerticalSlash, head
     vsc = torch.empty((n, s_len), dtype=torch.float64, device=dev) if with_scores else None
     ssc = torch.empty((n, s_len), dtype=torch.float64, device=dev) if with_scores else None
     flags = torch.empty(n, dtype=torch.int32, device=dev)
-    code = _lib.SPF_VS_FAST if mode == "fast" else _lib.SPF_VS_EXACT
+    codes = {"fast": _lib.SPF_VS_FAST, "exact": _lib.SPF_VS_EXACT, "uncertified": _lib.SPF_VS_FAST_UNCERTIFIED}
+    if mode not in codes:
+        raise ValueError(f"unknown estimation mode {mode!r}")
+    code = codes[mode]
     dt = _dtype_code(q)
     lib = _lib.load()
     ws_bytes = lib.spf_vs_estimate_workspace_size(code, dt, hq, hkv, n, s_len, d, cfg.last_q)

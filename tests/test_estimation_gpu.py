@@ -56,31 +56,30 @@ def test_vs_golden_scores_and_bf16_path(golden, P):
 @pytest.mark.parametrize("s,seed,gen", [(8192, 0, "iid"), (8192, 3, "iid"), (32768, 1, "iid"), (5000, 2, "iid"),
                                         (16384, 0, "local"), (131072, 0, "local")])
 def test_vs_tensor_core_error_model(P, s, seed, gen):
-    """The tensor-core scores stay well inside the certification threshold
-    (tau = 2^-20 (1 + max|s|), estimate_vs_tc.cu): measured max relative error
-    of the vertical / slash vectors vs the fp64 path, on all four heads of a
-    GQA group (Hq=4, Hkv=1)."""
+    """Measured error of the raw tensor-core vectors (mode "uncertified") against the
+    fp64 path, next to the rigorous bound eta of estimate_vs_tc.cu: the bound holds with
+    room to spare (it is a worst case, the measured error a typical one), and the
+    production path ("fast") selects exactly the fp64 sets on all four heads."""
     from benchmarks.workloads import g_iid_qkv, g_local_qkv
+
+    from test_headline_parity_gpu import _eta_bound
 
     gen_fn = g_iid_qkv if gen == "iid" else g_local_qkv
     q, k, _ = gen_fn(4, 1, s, 128, seed=seed, device="cuda")
     cfg = P.VerticalSlash(1000, 6096, 64)
     from paper_2407_02490_b200.estimator import vs_estimate_async
 
-    vf, sf, vsf, ssf, flags = vs_estimate_async(q, k, cfg, mode="fast", with_scores=True)
+    _, _, vsr, ssr, _ = vs_estimate_async(q, k, cfg, mode="uncertified", with_scores=True)
+    vf, sf, _, _, _ = vs_estimate_async(q, k, cfg, mode="fast")
     ve, se, vse, sse, _ = vs_estimate_async(q, k, cfg, mode="exact", with_scores=True)
-    qf = q.float()
-    smax = (qf[:, -64:] @ k[0].float().T).abs().max().item() / np.sqrt(128)
-    tau = 2.0 ** -20 * (1 + smax)
-    for fast, exact in ((vsf, vse), (ssf, sse)):
-        fast, exact = fast.cpu().numpy(), exact.cpu().numpy()
-        big = exact > 1e-20
-        rel = np.abs(fast[big] - exact[big]) / exact[big]
-        assert rel.max() < tau / 2, (gen, s, rel.max(), tau)
-    # certified heads select exactly the fp64 sets
+    etas = _eta_bound(q, k, 4, 1)
     for h in range(4):
-        if int(flags[h]) == 0:
-            assert torch.equal(vf[h], ve[h]) and torch.equal(sf[h], se[h]), h
+        for fast, exact in ((vsr[h], vse[h]), (ssr[h], sse[h])):
+            fast, exact = fast.cpu().numpy(), exact.cpu().numpy()
+            big = exact > 1e-30
+            rel = np.abs(fast[big] - exact[big]) / exact[big]
+            assert rel.max() <= etas[h], (gen, s, h, rel.max(), etas[h])
+    assert torch.equal(vf, ve) and torch.equal(sf, se)
 
 
 def test_vs_gqa_multihead_matches_port(P):

@@ -55,13 +55,16 @@ struct ExArgs {
   double2* row_ml;         // [n_heads][L]
   double* vscore;          // [n_heads][S]
   double* sscore;          // [n_heads][S]
-  int32_t* list;           // fallback: significant items (h * n_kblk + kb) of the flagged heads
-  int32_t* list_count;     // number of entries in list (device)
-  double* cache;           // fallback with L = KB = 64: pass A's scaled scores of list items [w][64][64]
-  int cache_items;         // items the cache holds (list positions >= this are recomputed)
+  // fallback (tile_max given, L = KB = 64): per flagged head the significant 64-key items,
+  // list[h * n_kblk + i] = kb for i < head_count[h] (any order)
+  int32_t* list;
+  int32_t* head_count;     // [n_heads]
+  uint8_t* sig;            // [n_heads][n_kblk]: item significant (prep), compacted in kb order by the list kernel
+  double* cache;           // pass A's scaled scores of the listed items, [virtual item][64][64]
+  int cache_items;         // items the cache holds (virtual items >= this are rescored in pass B)
 };
 
-constexpr int kCacheItems = 4096;  // 128 MB: the significant items of every flagged head at C2
+constexpr int kCacheItems = 8192;  // 256 MB: the significant items of 32 G-local heads at 128K-1M
 
 template <typename T>
 __device__ __forceinline__ double ld_f64(const T* p) {
@@ -150,8 +153,8 @@ __device__ bool item_significant(const ExArgs& a, int h, int k0) {
 }
 
 // Fallback preparation (tile_max given): one warp per (flagged head, 64-key item).
-// Zeroes the item's slash entries, writes the outputs of items whose probabilities
-// are all exactly 0 in fp32 (stats (-inf, 0), vertical 0) and lists the others.
+// Zeroes the item's slash entries, writes the vertical scores of items whose
+// probabilities are all exactly 0 in fp32 and flags the others.
 __global__ void vs_exact_prep_kernel(const ExArgs a) {
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -169,12 +172,30 @@ __global__ void vs_exact_prep_kernel(const ExArgs a) {
   }
   sig = __any_sync(0xffffffffu, sig);
   for (int o = k0 + lane; o < min(k0 + a.KB, S); o += 32) a.sscore[(int64_t)h * S + o] = 0.0;
-  if (sig) {
-    if (lane == 0) a.list[atomicAdd(a.list_count, 1)] = (int32_t)w;
-  } else {
-    for (int i = lane; i < a.L; i += 32) a.stats[((int64_t)h * a.L + i) * a.n_kblk + kb] = make_double2(-INFINITY, 0.0);
+  if (lane == 0) a.sig[w] = (uint8_t)(sig ? 1 : 0);
+  if (!sig)
     for (int j = k0 + lane; j < min(k0 + a.KB, S); j += 32) a.vscore[(int64_t)h * S + j] = 0.0;
+}
+
+// Per flagged head: the significant items in ascending kb order (a block scan of the
+// flags), so pass A's per-item statistics are combined in a fixed order.
+constexpr int kListThreads = 1024;
+__global__ void __launch_bounds__(kListThreads) vs_exact_list_kernel(const ExArgs a) {
+  using Scan = cub::BlockScan<int, kListThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int h = blockIdx.x;
+  if (a.gate != nullptr && a.gate[h] == 0) return;
+  int base = 0;
+  for (int c0 = 0; c0 < a.n_kblk; c0 += kListThreads) {
+    const int kb = c0 + threadIdx.x;
+    const int f = kb < a.n_kblk ? a.sig[(int64_t)h * a.n_kblk + kb] : 0;
+    int pos, tot;
+    Scan(tmp).ExclusiveSum(f, pos, tot);
+    if (f) a.list[(int64_t)h * a.n_kblk + base + pos] = kb;
+    base += tot;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) a.head_count[h] = base;
 }
 
 template <typename T, int kPass>
@@ -188,31 +209,21 @@ __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restri
   const int S = a.S, L = a.L, KB = a.KB, d = a.d;
   const int n_rt = (L + kRowT - 1) / kRowT;
   // items (head, key block) interleaved head-fastest, so the significant blocks of every
-  // flagged head (often a narrow band of keys) spread over all CTAs
-  // with a prepared list (fallback) only its items are visited; the prep kernel
-  // already zeroed the slash vector and wrote the skipped items' outputs
-  const bool listed = a.list != nullptr;
-  const int64_t n_items = listed ? (int64_t)*a.list_count : (int64_t)a.n_heads * a.n_kblk;
+  // head (often a narrow band of keys) spread over all CTAs
+  const int64_t n_items = (int64_t)a.n_heads * a.n_kblk;
   for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    int h, kb;
-    if (listed) {
-      const int it = a.list[w];
-      h = it / a.n_kblk;
-      kb = it % a.n_kblk;
-    } else {
-      h = (int)(w % a.n_heads);
-      kb = (int)(w / a.n_heads);
-    }
-    if (!listed && a.gate != nullptr && a.gate[h] == 0) continue;
+    const int h = (int)(w % a.n_heads);
+    const int kb = (int)(w / a.n_heads);
+    if (a.gate != nullptr && a.gate[h] == 0) continue;
     const int qh_id = a.head_ids ? a.head_ids[h] : h;
     const T* qh = q + ((int64_t)qh_id * S + (S - L)) * d;
     const T* kh = k + (int64_t)(qh_id / a.hpk) * S * d;
     {
       const int k0 = kb * KB;
-      if (kPass == 1 && !listed) {  // zero this item's share of the slash vector (pass 2 accumulates into it)
+      if (kPass == 1) {  // zero this item's share of the slash vector (pass 2 accumulates into it)
         for (int o = k0 + tid; o < min(k0 + KB, S); o += kThreads) a.sscore[(int64_t)h * S + o] = 0.0;
       }
-      const bool sig = listed || item_significant(a, h, k0);
+      const bool sig = item_significant(a, h, k0);
       if (!sig) {
         if (kPass == 1) {
           for (int i = tid; i < L; i += kThreads)
@@ -248,23 +259,7 @@ __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restri
         for (int sb = 0; sb < KB / kKeyT; ++sb) {
           const int kk0 = k0 + sb * kKeyT;
           double acc[4][4];
-          // pass B reuses pass A's fp64 scores of a listed item (bit-identical, no recompute)
-          const bool cached = listed && a.cache != nullptr && w < a.cache_items;
-          double* cw = cached ? a.cache + (size_t)w * (64 * 64) : nullptr;
-          if (kPass == 2 && cached) {
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-              for (int y = 0; y < 4; ++y) acc[x][y] = cw[(4 * tr + x) * 64 + tk + 16 * y];
-          } else {
-            score_tile(sm, qh, kh, r0, nrv, kk0, S, d, acc);
-            if (kPass == 1 && cached) {
-#pragma unroll
-              for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) cw[(4 * tr + x) * 64 + tk + 16 * y] = acc[x][y];
-            }
-          }
+          score_tile(sm, qh, kh, r0, nrv, kk0, S, d, acc);
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
             const int i = r0 + 4 * tr + x;
@@ -348,6 +343,252 @@ __global__ void __launch_bounds__(kThreads, 2) vs_exact_kernel(const T* __restri
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Fallback fp64 scoring on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64: 37 TF/s on this
+// B200 vs 30-34 for DFMA, benchmarks/mb_dmma.cu), for the flagged heads' listed items
+// (L = KB = 64, bf16 inputs, head_dim 64 / 128).  The work is the concatenation of the
+// heads' item lists ("virtual items"); CTA b takes a contiguous range of it, so the 64 tail
+// rows of Q (fp64 in shared memory) are staged once per head, and the next item's K rows
+// are fetched into registers while the current item is scored.  Per item the 64 x 64 fp64
+// scores are exact products of bf16 values summed in fp64 (DMMA, fixed order: bit-identical
+// across runs).  Pass A caches the scaled scores and writes per-(row, item) (max, sum exp);
+// pass B reads them back (or rescores items past the cache) and forms p, column and
+// diagonal sums exactly as vs_exact_kernel does.
+constexpr int kFbThreads = 256;
+
+template <int kD>
+struct FbSmem {
+  static constexpr int kLd = kD + 4;                // doubles per staged row (2-wavefront fragment loads)
+  static constexpr int kOffQ = 0;                   // double [64][kLd]
+  static constexpr int kOffK = kOffQ + 64 * kLd * 8;
+  static constexpr int kOffP = kOffK + 64 * kLd * 8;  // float [64][65] (pass B)
+  static constexpr int kOffCol = kOffP + 64 * 65 * 4;  // double [64]
+  static constexpr int kOffDiag = kOffCol + 64 * 8;    // double [127]
+  static constexpr int kOffRed = kOffDiag + 128 * 8;   // double [2][64] (cross-warp row reductions)
+  static constexpr int kOffOff = kOffRed + 2 * 64 * 8;  // int [kMaxFbHeads + 1]
+  static constexpr int kBytes = kOffOff + (1024 + 1) * 4;
+};
+constexpr int kMaxFbHeads = 1024;
+
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// 64 rows x kD bf16 -> fp64 rows of the staged matrix (rows past `valid` are zero)
+template <int kD>
+__device__ __forceinline__ void fb_fetch(const __nv_bfloat16* src, int valid, int4 (&r)[kD / 32]) {
+  // 64 rows x kD bf16 = 64 * kD / 8 16-byte chunks; thread t takes chunks t, t + 256, ...
+#pragma unroll
+  for (int u = 0; u < kD / 32; ++u) {
+    const int ch = threadIdx.x + u * kFbThreads;
+    const int row = ch / (kD / 8), c8 = ch % (kD / 8);
+    r[u] = row < valid ? *reinterpret_cast<const int4*>(src + (int64_t)row * kD + c8 * 8) : make_int4(0, 0, 0, 0);
+  }
+}
+template <int kD>
+__device__ __forceinline__ void fb_store(double* dst, const int4 (&r)[kD / 32]) {
+#pragma unroll
+  for (int u = 0; u < kD / 32; ++u) {
+    const int ch = threadIdx.x + u * kFbThreads;
+    const int row = ch / (kD / 8), c8 = ch % (kD / 8);
+    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&r[u]);
+    double2* o = reinterpret_cast<double2*>(dst + row * FbSmem<kD>::kLd + c8 * 8);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = make_double2(__bfloat162float(x[2 * e]), __bfloat162float(x[2 * e + 1]));
+  }
+}
+
+// acc[mi][ni] = 8x8 tiles of Q K^T: rows m0 + 8 mi (+ lane / 4), keys n0 + 8 ni (+ 2 (lane % 4) + {0, 1})
+template <int kD>
+__device__ __forceinline__ void fb_scores(const double* Qs, const double* Ks, int m0, int n0, double (&acc)[2][4][2]) {
+  constexpr int kLd = FbSmem<kD>::kLd;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const double* qa = Qs + (m0 + (lane >> 2)) * kLd + (lane & 3);
+  const double* kb = Ks + (n0 + (lane >> 2)) * kLd + (lane & 3);
+#pragma unroll 8
+  for (int ks = 0; ks < kD / 4; ++ks) {
+    double a[2], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) a[mi] = qa[mi * 8 * kLd + 4 * ks];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = kb[ni * 8 * kLd + 4 * ks];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_f64(acc[mi][ni], a[mi], b[ni]);
+  }
+}
+
+template <int kD, int kPass>
+__global__ void __launch_bounds__(kFbThreads, 1) vs_fb_kernel(const __nv_bfloat16* __restrict__ q,
+                                                              const __nv_bfloat16* __restrict__ k, const ExArgs a) {
+  using SM = FbSmem<kD>;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  double* Qs = reinterpret_cast<double*>(smraw + SM::kOffQ);
+  double* Ks = reinterpret_cast<double*>(smraw + SM::kOffK);
+  float(*Ps)[65] = reinterpret_cast<float(*)[65]>(smraw + SM::kOffP);
+  double* colsum = reinterpret_cast<double*>(smraw + SM::kOffCol);
+  double* red = reinterpret_cast<double*>(smraw + SM::kOffRed);
+  int* off = reinterpret_cast<int*>(smraw + SM::kOffOff);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = a.S, nh = a.n_heads;
+  if (tid == 0) {  // virtual item offsets of the heads' lists
+    int o = 0;
+    for (int h = 0; h < nh; ++h) {
+      off[h] = o;
+      o += (a.gate != nullptr && a.gate[h] == 0) ? 0 : a.head_count[h];
+    }
+    off[nh] = o;
+  }
+  __syncthreads();
+  const int total = off[nh];
+  const int u0 = (int)((int64_t)blockIdx.x * total / gridDim.x), u1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  if (u0 >= u1) return;
+  const int m0 = 16 * (warp >> 1), n0 = 32 * (warp & 1);  // warp's 16 rows x 32 keys of the item
+  int h = 0;
+  while (off[h + 1] <= u0) ++h;
+  int cur_q = -1, kreg_item = -1;
+  int4 kreg[kD / 32];
+  auto item_kb = [&](int u, int hh) { return a.list[(int64_t)hh * a.n_kblk + (u - off[hh])]; };
+  auto head_kbase = [&](int hh) {
+    const int qh = a.head_ids ? a.head_ids[hh] : hh;
+    return k + (int64_t)(qh / a.hpk) * S * kD;
+  };
+  auto needs_scores = [&](int u) { return kPass == 1 || a.cache == nullptr || u >= a.cache_items; };
+  for (int u = u0; u < u1; ++u) {
+    while (off[h + 1] <= u) ++h;
+    const int kb = item_kb(u, h);
+    const int k0 = kb * 64;
+    double acc[2][4][2];
+    if (needs_scores(u)) {
+      if (kreg_item != u) fb_fetch<kD>(head_kbase(h) + (int64_t)k0 * kD, min(64, S - k0), kreg);
+      __syncthreads();  // previous item's readers of Qs / Ks are done
+      if (cur_q != h) {
+        const int qh = a.head_ids ? a.head_ids[h] : h;
+        int4 qreg[kD / 32];
+        fb_fetch<kD>(q + ((int64_t)qh * S + (S - 64)) * kD, 64, qreg);
+        fb_store<kD>(Qs, qreg);
+        cur_q = h;
+      }
+      fb_store<kD>(Ks, kreg);
+      __syncthreads();
+      // prefetch the next item's keys while this one is scored
+      if (u + 1 < u1 && needs_scores(u + 1)) {
+        int hn = h;
+        while (off[hn + 1] <= u + 1) ++hn;
+        const int kbn = item_kb(u + 1, hn);
+        fb_fetch<kD>(head_kbase(hn) + (int64_t)kbn * 64 * kD, min(64, S - kbn * 64), kreg);
+        kreg_item = u + 1;
+      }
+      fb_scores<kD>(Qs, Ks, m0, n0, acc);
+    }
+    double* cw = (a.cache != nullptr && u < a.cache_items) ? a.cache + (size_t)u * (64 * 64) : nullptr;
+    // scaled, causally masked scores of this thread's 16 cells
+    double s[2][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = m0 + 8 * mi + (lane >> 2), jl = n0 + 8 * ni + 2 * (lane & 3) + e;
+          double x;
+          if (kPass == 2 && !needs_scores(u)) {
+            x = cw[i * 64 + jl];
+          } else {
+            const bool valid = k0 + jl <= S - 64 + i;  // causal (also excludes keys >= S)
+            x = valid ? a.scale * acc[mi][ni][e] : -INFINITY;
+            if (kPass == 1 && cw != nullptr) cw[i * 64 + jl] = x;
+          }
+          s[mi][ni][e] = x;
+        }
+    if (kPass == 1) {
+      // per row: max and sum exp over the item's 64 keys (4 lanes x 2 warps hold a row)
+      double mx[2], l[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        double m = -INFINITY;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) m = fmax(m, fmax(s[mi][ni][0], s[mi][ni][1]));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        mx[mi] = m;
+      }
+      if ((lane & 3) == 0) {
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) red[(warp & 1) * 64 + m0 + 8 * mi + (lane >> 2)] = mx[mi];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int i = m0 + 8 * mi + (lane >> 2);
+        mx[mi] = fmax(red[i], red[64 + i]);
+        double acc_l = 0.0;
+        if (mx[mi] != -INFINITY) {
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (s[mi][ni][e] != -INFINITY) acc_l += exp(s[mi][ni][e] - mx[mi]);
+        }
+        acc_l += __shfl_xor_sync(0xffffffffu, acc_l, 1);
+        acc_l += __shfl_xor_sync(0xffffffffu, acc_l, 2);
+        l[mi] = acc_l;
+      }
+      __syncthreads();  // row maxima read: red is reused for the sums
+      if ((lane & 3) == 0) {
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) red[(warp & 1) * 64 + m0 + 8 * mi + (lane >> 2)] = l[mi];
+      }
+      __syncthreads();
+      if ((warp & 1) == 0 && (lane & 3) == 0) {
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int i = m0 + 8 * mi + (lane >> 2);
+          // indexed by list position: the combine visits only the listed items, in kb order
+          a.stats[((int64_t)h * 64 + i) * a.n_kblk + (u - off[h])] = make_double2(mx[mi], red[i] + red[64 + i]);
+        }
+      }
+    } else {
+      // p = fp32(exp(s - m_i) / l_i) (tensor.py:78); column sums over rows ascending and
+      // diagonal sums as vs_exact_kernel (est.sum(axis=0) / np.bincount orders)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int i = m0 + 8 * mi + (lane >> 2);
+        const double2 ml = a.row_ml[(int64_t)h * 64 + i];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double x = s[mi][ni][e];
+            Ps[i][n0 + 8 * ni + 2 * (lane & 3) + e] = x == -INFINITY ? 0.f : __double2float_rn(exp(x - ml.x) / ml.y);
+          }
+      }
+      __syncthreads();
+      if (tid < 64) {
+        double cs = 0.0;
+        for (int ii = 0; ii < 64; ++ii) cs += (double)Ps[ii][tid];
+        if (k0 + tid < S) a.vscore[(int64_t)h * S + k0 + tid] = cs;
+      }
+      // diagonal cl = key - row in [-63, 63]; offset o = (S - 64 + row) - (k0 + key)
+      for (int cl = tid - 63; cl <= 63; cl += kFbThreads) {
+        const int ii0 = max(0, -cl), ii1 = min(64, 64 - cl);
+        double ds = 0.0;
+        for (int ii = ii0; ii < ii1; ++ii) ds += (double)Ps[ii][ii + cl];
+        const int o = S - 64 - k0 - cl;
+        if (o >= 0 && o < S && ds != 0.0) atomicAdd(a.sscore + (int64_t)h * S + o, ds);
+      }
+      __syncthreads();  // Ps is rewritten by the next item
+    }
+  }
+}
+
 // (m_i, l_i) from the item partials: one warp per (head, row), lane-strided then a
 // fixed butterfly, so the order is deterministic.
 __global__ void vs_exact_combine_kernel(const ExArgs a) {
@@ -357,12 +598,14 @@ __global__ void vs_exact_combine_kernel(const ExArgs a) {
   const int lane = threadIdx.x & 31;
   if (i >= a.L) return;
   const double2* st = a.stats + ((int64_t)h * a.L + i) * a.n_kblk;
+  // fallback: the listed items' statistics (by list position); otherwise every item's
+  const int n_st = a.head_count != nullptr ? a.head_count[h] : a.n_kblk;
   double m = -INFINITY;
-  for (int b = lane; b < a.n_kblk; b += 32) m = fmax(m, st[b].x);
+  for (int b = lane; b < n_st; b += 32) m = fmax(m, st[b].x);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   double l = 0.0;
-  for (int b = lane; b < a.n_kblk; b += 32) {
+  for (int b = lane; b < n_st; b += 32) {
     const double2 v = st[b];
     if (v.x != -INFINITY) l += v.y * exp(v.x - m);
   }
@@ -405,7 +648,8 @@ size_t vs_exact_workspace_size(int n_heads, int seq_len, int last_q) {
   const int KB = kb_for(last_q);
   const size_t n_kblk = (seq_len + KB - 1) / KB;
   return al256((size_t)n_heads * last_q * n_kblk * 16) + al256((size_t)n_heads * last_q * 16) +
-         2 * al256((size_t)n_heads * seq_len * 8) + al256((size_t)n_heads * n_kblk * 4) + al256(4) +
+         2 * al256((size_t)n_heads * seq_len * 8) + al256((size_t)n_heads * n_kblk * 4) + al256((size_t)n_heads * 4) +
+         al256((size_t)n_heads * n_kblk) +
          al256((size_t)cache_items_for(n_heads, seq_len, last_q) * 64 * 64 * 8);
 }
 
@@ -440,12 +684,51 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
   a.vscore = vscore ? vscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   a.sscore = sscore ? sscore : reinterpret_cast<double*>(take((size_t)n_heads * S * 8));
   int32_t* list = reinterpret_cast<int32_t*>(take((size_t)n_heads * a.n_kblk * 4));
-  int32_t* list_count = reinterpret_cast<int32_t*>(take(4));
+  int32_t* head_count = reinterpret_cast<int32_t*>(take((size_t)n_heads * 4));
+  uint8_t* sig = take((size_t)n_heads * a.n_kblk);
   const int cache_items = cache_items_for(n_heads, S, L);
   double* cache = reinterpret_cast<double*>(take((size_t)cache_items * 64 * 64 * 8));
   const size_t smem = sizeof(ExSmem) + (size_t)(2 * a.KB + L - 1) * 8;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)a.n_kblk * n_heads, 148 * 4));
   int rc;
+  const bool fallback = tile_max != nullptr && L == 64 && a.KB == 64 && dtype == SPF_DTYPE_BF16 &&
+                        (d == 64 || d == 128) && n_heads <= kMaxFbHeads;
+  if (fallback) {
+    // flagged heads only: list their significant items, score them on the fp64 tensor cores
+    a.list = list;
+    a.sig = sig;
+    a.head_count = head_count;
+    a.cache = cache_items > 0 ? cache : nullptr;
+    a.cache_items = cache_items;
+    const int64_t warps = (int64_t)n_heads * a.n_kblk;
+    auto k1 = d == 128 ? vs_fb_kernel<128, 1> : vs_fb_kernel<64, 1>;
+    auto k2 = d == 128 ? vs_fb_kernel<128, 2> : vs_fb_kernel<64, 2>;
+    const int fb_smem = d == 128 ? FbSmem<128>::kBytes : FbSmem<64>::kBytes;
+    static bool fb_attr = false;
+    if (!fb_attr) {
+      for (auto kk : {vs_fb_kernel<128, 1>, vs_fb_kernel<128, 2>})
+        if ((rc = check_cuda(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  FbSmem<128>::kBytes), "vs fallback smem")))
+          return rc;
+      for (auto kk : {vs_fb_kernel<64, 1>, vs_fb_kernel<64, 2>})
+        if ((rc = check_cuda(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  FbSmem<64>::kBytes), "vs fallback smem")))
+          return rc;
+      fb_attr = true;
+    }
+    const auto* qb = reinterpret_cast<const __nv_bfloat16*>(q);
+    const auto* kbp = reinterpret_cast<const __nv_bfloat16*>(k);
+    note_launches(6);  // prep, list, pass A, combine, pass B, top-k
+    vs_exact_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+    vs_exact_list_kernel<<<(unsigned)n_heads, kListThreads, 0, st>>>(a);
+    k1<<<148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
+    vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
+    k2<<<148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
+    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
+                                                                                      k_s, gate, vout, sout);
+    return check_cuda(cudaGetLastError(), "vs fallback");
+  }
+  a.tile_max = nullptr;  // the full fp64 path visits every item
   auto launch = [&](auto k1, auto k2, const auto* qq, const auto* kk) {
     if ((rc = check_cuda(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          "vs exact smem")))
@@ -454,16 +737,6 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
                          "vs exact smem")))
       return rc;
     note_launches(4);  // pass A, combine, pass B, top-k
-    if (a.tile_max != nullptr) {
-      if ((rc = check_cuda(cudaMemsetAsync(list_count, 0, 4, st), "list count"))) return rc;
-      a.list = list;
-      a.list_count = list_count;
-      a.cache = cache_items > 0 ? cache : nullptr;
-      a.cache_items = cache_items;
-      const int64_t warps = (int64_t)n_heads * a.n_kblk;
-      note_launches(1);
-      vs_exact_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
-    }
     k1<<<grid, kThreads, smem, st>>>(qq, kk, a);
     vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
     k2<<<grid, kThreads, smem, st>>>(qq, kk, a);

@@ -571,10 +571,22 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
     const int i = r % kTailRows;
     a.row_mc[(int64_t)slot[mm] * kTailRows + i] = m;
     // E_i = gamma * sum_c |q_ic| max_j |k_jc| (fp64: exact products of bf16 values, tiny sum error)
-    const __nv_bfloat16* qr = q + ((int64_t)head[mm] * a.S + (a.S - kTailRows + i)) * kD;
-    double sabs = 0.0;
-    for (int c = 0; c < kD; ++c) sabs += fabs((double)__bfloat162float(qr[c])) * (double)kabs_s[c];
-    const double e_i = score_gamma<kD>() * sabs * (1.0 + 0x1p-40);
+    // (fp32: bf16 x bf16 products are exact, kD positive terms err by < kD 2^-24 relative)
+    const int4* qr = reinterpret_cast<const int4*>(q + ((int64_t)head[mm] * a.S + (a.S - kTailRows + i)) * kD);
+    float sa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int c8 = 0; c8 < kD / 8; ++c8) {
+      const int4 x = __ldg(qr + c8);
+      const uint32_t w[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t ab = w[e] & 0x7fff7fffu;
+        sa[e] = fmaf(__uint_as_float(ab << 16), kabs_s[c8 * 8 + 2 * e], sa[e]);
+        sa[e] = fmaf(__uint_as_float(ab & 0xffff0000u), kabs_s[c8 * 8 + 2 * e + 1], sa[e]);
+      }
+    }
+    const double sabs = ((double)sa[0] + sa[1]) + ((double)sa[2] + sa[3]);
+    const double e_i = score_gamma<kD>() * sabs * (1.0 + 0x1p-15);
     err = (float)(e_i * (1.0 + 0x1p-20));
     // fp64 path: an item is skipped when its tensor-core scores sit > 151 + marg (log2 units)
     // below the row max; the true scores can be E_i higher and the true max E_i lower

@@ -544,309 +544,176 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     int t = 0;
-    if constexpr (kSepP<kSplit>) {
-      // bf16 path, software-pipelined: step t+1's descriptor wait and S load are issued
-      // right after P(t)'s store, so their latencies (~570 cycles measured) overlap the
-      // row sum, the rare O rescale and the P store wait instead of following them.
-      uint32_t x[kBox];
-      int kind = kEnd, lo = 0, hi = 0;
-      auto fetch = [&](int tt, int& kd, int& lo_o, int& hi_o) {
-        const int sd = tt % R::kD;
-        mbar_wait(&ctrl->d_full[sd], (tt / R::kD) & 1);
-        const StepDesc& d = ctrl->desc[sd];
-        kd = d.kind;
-        if (kd == kEnd) return;
-        mbar_wait(&ctrl->s_full[0], tt & 1);
-        tc_fence_after();
-        tmem_ld32x32b_x64(tmem + lane_off, x);  // S(tt) -> x (completes at the next wait::ld)
-        // valid key slots for this row, [lo, hi), computed while the TMEM load is in flight
-        lo_o = 0;
-        hi_o = 0;
-        if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
-          if (kd == kTile) {
-            lo_o = max(0, -d.box);
-            hi_o = min((int)d.width, min(S - d.box, q - d.box + 1));
-          } else {
-            int a0 = 0, b0 = d.width;
-            while (a0 < b0) {
-              const int m = (a0 + b0) >> 1;
-              if (d.pmax[m] <= q) a0 = m + 1; else b0 = m;
-            }
-            hi_o = a0;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
-      };
-      fetch(0, kind, lo, hi);
-      for (; kind != kEnd; ++t) {
-        const int sb = t & 1;  // P buffer
-        const uint32_t pcol = kBox + sb * (kBox / 2);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ctrl->s_free[0]);  // S(t) consumed: QK(t+1) may overwrite it
-        float alpha = 1.f, sum = 0.f;
-        bool rescale = false;
-        uint32_t ph[kBox / 2];
-        if (!__any_sync(0xffffffffu, hi > lo)) {
-          // none of this warp's rows sees the step (the other row block's tile of a union
-          // step, a block-sparse block of the other row): P = 0, softmax state unchanged
-#pragma unroll
-          for (int j = 0; j < kBox / 2; ++j) ph[j] = 0u;
-        } else {
-          // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
-          if (!(lo == 0 && hi == kBox)) {
-#pragma unroll
-            for (int j = 0; j < kBox; ++j) x[j] = (j >= lo && j < hi) ? x[j] : 0xff800000u;
-          }
-          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-          for (int j = 0; j < kBox; j += 8) {
-            mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
-            mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
-            mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
-            mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
-          }
-          const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
-          if (hi > lo) {
-            const float m_tile = mx * scale_log2;
-            if (m_run == -INFINITY) {
-              m_run = m_tile;
-            } else if (m_tile > m_run + 8.f) {
-              alpha = exp2f(m_run - m_tile);
-              m_run = m_tile;
-              rescale = true;
-            }
-          }
-          // p = 2^(x*c - m): packed FFMA2, MUFU ex2, packed FADD2 row sums
-          const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
-          const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
-          const uint64_t m2 = pack_f32x2(neg_m, neg_m);
-          uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-#pragma unroll
-          for (int j = 0; j < kBox; j += 2) {
-            const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
-            float y0, y1;
-            unpack_f32x2(yv, y0, y1);
-            const float p0 = ex2_approx(y0);
-            const float p1 = ex2_approx(y1);
-            const uint64_t pp = pack_f32x2(p0, p1);
-            switch ((j >> 1) & 3) {
-              case 0: s0 = fadd2(s0, pp); break;
-              case 1: s1 = fadd2(s1, pp); break;
-              case 2: s2 = fadd2(s2, pp); break;
-              default: s3 = fadd2(s3, pp); break;
-            }
-            ph[j >> 1] = pack_bf16x2(p0, p1);
-          }
-          float sa, sb2;
-          unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
-          sum = sa + sb2;
-        }
-        // P(t) -> TMEM (bf16 pairs, K-major; PV reads A from TMEM).  Its buffer was last read
-        // by PV(t-2), retired before QK(t) completed.
-        tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
-        // next step's descriptor and S load (x is free: its exponentials are in ph)
-        int kind_n = kEnd, lo_n = 0, hi_n = 0;
-        fetch(t + 1, kind_n, lo_n, hi_n);
-        l_run = l_run * alpha + sum;
-        // O rescale needs PV(t-1) retired: the V slot it read is released by a commit behind it
-        // (v_empty, phase (t-1)/kV); S(t) ready implies PV(t-2) retired, so the parity wait
-        // cannot alias.  tcgen05.ld/st are warp-collective: decide per warp.  (Its wait::ld also
-        // completes S(t+1)'s load, which is harmless.)
-        if (t > 0 && __any_sync(0xffffffffu, rescale)) {
-          mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < kD; c += 32) {
-            uint32_t o[32];
-            tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-            tmem_st32x32b_x32(tmem + lane_off + 128 + c, o);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&ctrl->p_full[sb]);
-        kind = kind_n;
-        lo = lo_n;
-        hi = hi_n;
-      }
-    } else {
     for (;; ++t) {
-        const int sd = t % R::kD;
-        mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
-        const StepDesc& d = ctrl->desc[sd];
-        const int kind = d.kind;
-        if (kind == kEnd) break;
-        const int sb = t & 1;  // S buffer (split) / P buffer
-        if (kSepP<kSplit>) {
-          mbar_wait(&ctrl->s_full[0], t & 1);
+      const int sd = t % R::kD;
+      mbar_wait(&ctrl->d_full[sd], (t / R::kD) & 1);
+      const StepDesc& d = ctrl->desc[sd];
+      const int kind = d.kind;
+      if (kind == kEnd) break;
+      const int sb = t & 1;  // S buffer (split) / P buffer
+      if (kSepP<kSplit>) {
+        mbar_wait(&ctrl->s_full[0], t & 1);
+      } else {
+        mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
+      }
+      tc_fence_after();
+      const uint32_t s_col = kSepP<kSplit> ? 0u : (uint32_t)(sb * kBox);
+      uint32_t x[kCols];                          // own keys c0 .. c0+kCols-1
+      uint32_t y[kHalves > 1 ? kBox - kCols : 1];  // the other half (max only)
+      if (kHalves == 1) {
+        tmem_ld32x32b_x64(tmem + lane_off + s_col, x);
+      } else {
+        tmem_ld32x32b_x32(tmem + lane_off + s_col + c0, x);
+        tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
+      }
+      // valid key slots for this row, [lo, hi), computed while the TMEM load is in flight
+      int lo = 0, hi = 0;
+      if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
+        if (kind == kTile) {
+          lo = max(0, -d.box);
+          hi = min(d.width, min(S - d.box, q - d.box + 1));
         } else {
-          mbar_wait(&ctrl->s_full[sb], (t >> 1) & 1);
-        }
-        tc_fence_after();
-        const uint32_t s_col = kSepP<kSplit> ? 0u : (uint32_t)(sb * kBox);
-        uint32_t x[kCols];                          // own keys c0 .. c0+kCols-1
-        uint32_t y[kHalves > 1 ? kBox - kCols : 1];  // the other half (max only)
-        if (kHalves == 1) {
-          tmem_ld32x32b_x64(tmem + lane_off + s_col, x);
-        } else {
-          tmem_ld32x32b_x32(tmem + lane_off + s_col + c0, x);
-          tmem_ld32x32b_x32(tmem + lane_off + s_col + (c0 ^ kCols), y);
-        }
-        // valid key slots for this row, [lo, hi), computed while the TMEM load is in flight
-        int lo = 0, hi = 0;
-        if (seg >= 0 && ((d.segmask >> seg) & 1ull)) {
-          if (kind == kTile) {
-            lo = max(0, -d.box);
-            hi = min(d.width, min(S - d.box, q - d.box + 1));
-          } else {
-            int a = 0, b = d.width;
-            while (a < b) {
-              const int m = (a + b) >> 1;
-              if (d.pmax[m] <= q) a = m + 1; else b = m;
-            }
-            hi = a;
+          int a = 0, b = d.width;
+          while (a < b) {
+            const int m = (a + b) >> 1;
+            if (d.pmax[m] <= q) a = m + 1; else b = m;
           }
+          hi = a;
         }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
+      tmem_wait_ld();
+      if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctrl->d_empty[sd]);  // descriptor consumed (MMA read its kind earlier)
-        tmem_wait_ld();
-        if (kSepP<kSplit>) {  // S consumed: QK(t+1) may overwrite it while this step computes
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctrl->s_free[0]);
-        }
-        if (!__any_sync(0xffffffffu, hi > lo)) {
-          // none of this warp's rows sees the step (the other row block's tile of a union
-          // step, a block-sparse block of the other row): P = 0, softmax state unchanged
-          uint32_t z[32];
-  #pragma unroll
-          for (int j = 0; j < 32; ++j) z[j] = 0u;
-          if (kSepP<kSplit>) {
-            const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
-            if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, z);
-            else tmem_st32x32b_x32(tmem + lane_off + pcol, z);
-          } else {
-            tmem_st32x32b_x32(tmem + lane_off + sb * kBox, z);
-            if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, z);
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&ctrl->p_full[sb]);
-          continue;
-        }
-        // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
-        if (!(lo == 0 && hi == kBox)) {
-          const int xl = lo - c0, xh = hi - c0;
-  #pragma unroll
-          for (int j = 0; j < kCols; ++j) x[j] = (j >= xl && j < xh) ? x[j] : 0xff800000u;
-          if (kHalves > 1) {
-            const int yl = lo - (c0 ^ kCols), yh = hi - (c0 ^ kCols);
-  #pragma unroll
-            for (int j = 0; j < kBox - kCols; ++j) y[j] = (j >= yl && j < yh) ? y[j] : 0xff800000u;
-          }
-        }
-        // row max over all 64 keys: four independent 3-input max chains (FMNMX3)
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-  #pragma unroll
-        for (int j = 0; j < kCols; j += 8) {
-          mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
-          mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
-          mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
-          mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
-        }
-        if (kHalves > 1) {
-  #pragma unroll
-          for (int j = 0; j < kBox - kCols; j += 8) {
-            mx0 = fmax3(mx0, u2f(y[j]), u2f(y[j + 1]));
-            mx1 = fmax3(mx1, u2f(y[j + 2]), u2f(y[j + 3]));
-            mx2 = fmax3(mx2, u2f(y[j + 4]), u2f(y[j + 5]));
-            mx3 = fmax3(mx3, u2f(y[j + 6]), u2f(y[j + 7]));
-          }
-        }
-        const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
-        float alpha = 1.f;
-        bool rescale = false;
-        if (hi > lo) {
-          const float m_tile = mx * scale_log2;
-          if (m_run == -INFINITY) {
-            m_run = m_tile;
-          } else if (m_tile > m_run + 8.f) {
-            alpha = exp2f(m_run - m_tile);
-            m_run = m_tile;
-            rescale = true;
-          }
-        }
-        uint32_t ph[kCols / 2];
-        uint32_t pl[kSplit ? kCols / 2 : 1];
-        // p = 2^(x*c - m): packed FFMA2, MUFU ex2, packed FADD2 row sums
-        const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
-        const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
-        const uint64_t m2 = pack_f32x2(neg_m, neg_m);
-        uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-  #pragma unroll
-        for (int j = 0; j < kCols; j += 2) {
-          const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
-          float y0, y1;
-          unpack_f32x2(yv, y0, y1);
-          const float p0 = ex2_approx(y0);
-          const float p1 = ex2_approx(y1);
-          const uint64_t pp = pack_f32x2(p0, p1);
-          switch ((j >> 1) & 3) {
-            case 0: s0 = fadd2(s0, pp); break;
-            case 1: s1 = fadd2(s1, pp); break;
-            case 2: s2 = fadd2(s2, pp); break;
-            default: s3 = fadd2(s3, pp); break;
-          }
-          ph[j >> 1] = pack_bf16x2(p0, p1);
-          if (kSplit) {
-            const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&ph[j >> 1]);
-            const float2 hf = __bfloat1622float2(hb);
-            pl[j >> 1] = pack_bf16x2(p0 - hf.x, p1 - hf.y);
-          }
-        }
-        float sa, sb2;
-        unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
-        const float sum = sa + sb2;
-        l_run = l_run * alpha + sum;
-  
-        // O rescale needs PV(t-1) retired: the V slot it read is released by a commit behind
-        // it (v_empty, phase (t-1)/kV).  S(t) being ready implies PV(t-2) retired (QK(t) is
-        // issued after PV(t-2) and the commit behind s_full tracks every earlier MMA of the
-        // issuing thread), so that slot's previous phase (PV(t-1-kV)) is complete and the
-        // parity wait cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
-        // tcgen05.ld/st are warp-collective: decide per warp.
-        if (t > 0 && __any_sync(0xffffffffu, rescale)) {
-          mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
-          tc_fence_after();
-  #pragma unroll
-          for (int c = 0; c < kOCols; c += 32) {
-            uint32_t o[32];
-            tmem_ld32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
-            tmem_wait_ld();
-  #pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
-            tmem_st32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
-          }
-        }
-        // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
+        if (lane == 0) mbar_arrive(&ctrl->s_free[0]);
+      }
+      if (!__any_sync(0xffffffffu, hi > lo)) {
+        // none of this warp's rows sees the step (the other row block's tile of a union
+        // step, a block-sparse block of the other row): P = 0, softmax state unchanged
+        uint32_t z[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = 0u;
         if (kSepP<kSplit>) {
           const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
-          if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);
-          else tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
+          if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, z);
+          else tmem_st32x32b_x32(tmem + lane_off + pcol, z);
         } else {
-          tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
-          if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+          tmem_st32x32b_x32(tmem + lane_off + sb * kBox, z);
+          if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, z);
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&ctrl->p_full[sb]);
+        continue;
       }
+      // branch-free masking: invalid slots become -inf (ex2(-inf) = +0)
+      if (!(lo == 0 && hi == kBox)) {
+        const int xl = lo - c0, xh = hi - c0;
+#pragma unroll
+        for (int j = 0; j < kCols; ++j) x[j] = (j >= xl && j < xh) ? x[j] : 0xff800000u;
+        if (kHalves > 1) {
+          const int yl = lo - (c0 ^ kCols), yh = hi - (c0 ^ kCols);
+#pragma unroll
+          for (int j = 0; j < kBox - kCols; ++j) y[j] = (j >= yl && j < yh) ? y[j] : 0xff800000u;
+        }
+      }
+      // row max over all 64 keys: four independent 3-input max chains (FMNMX3)
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kCols; j += 8) {
+        mx0 = fmax3(mx0, u2f(x[j]), u2f(x[j + 1]));
+        mx1 = fmax3(mx1, u2f(x[j + 2]), u2f(x[j + 3]));
+        mx2 = fmax3(mx2, u2f(x[j + 4]), u2f(x[j + 5]));
+        mx3 = fmax3(mx3, u2f(x[j + 6]), u2f(x[j + 7]));
+      }
+      if (kHalves > 1) {
+#pragma unroll
+        for (int j = 0; j < kBox - kCols; j += 8) {
+          mx0 = fmax3(mx0, u2f(y[j]), u2f(y[j + 1]));
+          mx1 = fmax3(mx1, u2f(y[j + 2]), u2f(y[j + 3]));
+          mx2 = fmax3(mx2, u2f(y[j + 4]), u2f(y[j + 5]));
+          mx3 = fmax3(mx3, u2f(y[j + 6]), u2f(y[j + 7]));
+        }
+      }
+      const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+      float alpha = 1.f;
+      bool rescale = false;
+      if (hi > lo) {
+        const float m_tile = mx * scale_log2;
+        if (m_run == -INFINITY) {
+          m_run = m_tile;
+        } else if (m_tile > m_run + 8.f) {
+          alpha = exp2f(m_run - m_tile);
+          m_run = m_tile;
+          rescale = true;
+        }
+      }
+      uint32_t ph[kCols / 2];
+      uint32_t pl[kSplit ? kCols / 2 : 1];
+      // p = 2^(x*c - m): packed FFMA2, MUFU ex2, packed FADD2 row sums
+      const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+      const uint64_t c2 = pack_f32x2(scale_log2, scale_log2);
+      const uint64_t m2 = pack_f32x2(neg_m, neg_m);
+      uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+      for (int j = 0; j < kCols; j += 2) {
+        const uint64_t yv = ffma2(pack_f32x2(u2f(x[j]), u2f(x[j + 1])), c2, m2);
+        float y0, y1;
+        unpack_f32x2(yv, y0, y1);
+        const float p0 = ex2_approx(y0);
+        const float p1 = ex2_approx(y1);
+        const uint64_t pp = pack_f32x2(p0, p1);
+        switch ((j >> 1) & 3) {
+          case 0: s0 = fadd2(s0, pp); break;
+          case 1: s1 = fadd2(s1, pp); break;
+          case 2: s2 = fadd2(s2, pp); break;
+          default: s3 = fadd2(s3, pp); break;
+        }
+        ph[j >> 1] = pack_bf16x2(p0, p1);
+        if (kSplit) {
+          const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&ph[j >> 1]);
+          const float2 hf = __bfloat1622float2(hb);
+          pl[j >> 1] = pack_bf16x2(p0 - hf.x, p1 - hf.y);
+        }
+      }
+      float sa, sb2;
+      unpack_f32x2(fadd2(fadd2(s0, s1), fadd2(s2, s3)), sa, sb2);
+      const float sum = sa + sb2;
+      l_run = l_run * alpha + sum;
+
+      // O rescale needs PV(t-1) retired: the V slot it read is released by a commit behind
+      // it (v_empty, phase (t-1)/kV).  S(t) being ready implies PV(t-2) retired (QK(t) is
+      // issued after PV(t-2) and the commit behind s_full tracks every earlier MMA of the
+      // issuing thread), so that slot's previous phase (PV(t-1-kV)) is complete and the
+      // parity wait cannot alias.  The same fact frees P buffer t&1 (last read by PV(t-2)).
+      // tcgen05.ld/st are warp-collective: decide per warp.
+      if (t > 0 && __any_sync(0xffffffffu, rescale)) {
+        mbar_wait(&ctrl->v_empty[(t - 1) % R::kV], ((t - 1) / R::kV) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kOCols; c += 32) {
+          uint32_t o[32];
+          tmem_ld32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(u2f(o[j]) * alpha);
+          tmem_st32x32b_x32(tmem + lane_off + 128 + oc0 + c, o);
+        }
+      }
+      // P(t) -> TMEM: bf16 pairs, K-major (PV reads A from TMEM)
+      if (kSepP<kSplit>) {
+        const uint32_t pcol = kBox + sb * (kBox / 2) + half * (kCols / 2);
+        if (kCols == 32) tmem_st32x32b_x16(tmem + lane_off + pcol, ph);
+        else tmem_st32x32b_x32(tmem + lane_off + pcol, ph);
+      } else {
+        tmem_st32x32b_x32(tmem + lane_off + sb * kBox, ph);
+        if (kSplit) tmem_st32x32b_x32(tmem + lane_off + sb * kBox + 32, pl);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&ctrl->p_full[sb]);
     }
     // ---- epilogue: O / l -> global ----
     if (t > 0) {

@@ -53,6 +53,34 @@ def test_table_validation(P):
     assert t.block_size(0) == 32 and t.block_size(1) == 64
 
 
+def _check_against_oracle(out, q, k, v, cfgs, b):
+    import math
+
+    import numpy as np
+
+    import paper_2407_02490_b200 as P
+    from oracle import port
+
+    hq, s, d = q.shape
+    hkv = k.shape[0]
+    qn, kn, vn = (x.float().cpu().numpy() for x in (q, k, v))
+    got = out.float().cpu().numpy()
+    for h, cfg in enumerate(cfgs):
+        kvh = h // (hq // hkv)
+        if isinstance(cfg, P.VerticalSlash):
+            vv, ss = port.estimate_vertical_slash(qn[h], kn[kvh], cfg.k_v, cfg.k_s, cfg.last_q)
+            t, to, c, co = port.build_vs_csr(vv, ss, s, b)
+        else:
+            if isinstance(cfg, P.AShape):
+                tiles = port.a_shape_layout(s, cfg.global_tokens, cfg.local_window, b)
+            else:
+                tiles = port.block_rows_to_tiles(port.estimate_block_sparse(qn[h], kn[kvh], cfg.k_b, b), b)
+            t, to = port.flatten(tiles)
+            c, co = np.zeros(0, np.int64), np.zeros(len(to), np.int64)
+        want = port.sparse_flash_rows(qn[h], kn[kvh], vn[kvh], 1 / math.sqrt(d), b, t, to, c, co)
+        assert float(np.abs(got[h] - want).max()) < 2e-2, (h, cfg)
+
+
 @pytest.mark.gpu
 def test_driver_matches_layer_pipeline(P):
     import torch
@@ -70,6 +98,8 @@ def test_driver_matches_layer_pipeline(P):
     for l, (q, k, v) in enumerate(layers):
         want = P.sparse_prefill_attention(q, k, v, table.layer(l), 64)
         assert torch.equal(outs[l], want)
+        # and every head against the CPU oracle (estimation, merge / A-shape / BS tiles, kernel)
+        _check_against_oracle(outs[l], q, k, v, table.layer(l), 64)
     with pytest.raises(ValueError):
         SparsePrefill(table).layer(0, layers[0][0][:4].contiguous(), layers[0][1], layers[0][2])
 

@@ -61,3 +61,54 @@ def test_vertical_slash_prefill_runs(model_and_ids):
     ref = _logits(model, ids, "sdpa")
     # random weights give near-uniform attention, so the sparse output differs, but not wildly
     assert (got - ref).abs().mean().item() < 0.5 * ref.abs().mean().item() + 1e-3
+
+
+def test_sparse_hook_equals_oracle_per_head(model_and_ids, monkeypatch):
+    """The attention the hook computes inside the model (layer 0, per-head VS / BS patterns)
+    equals the CPU oracle of the reference's run_head on the same q / k / v, head by head:
+    layouts from the oracle's estimation + merge, outputs from the oracle kernel."""
+    import math
+
+    import numpy as np
+
+    from oracle import port
+    from paper_2407_02490_b200 import hf
+    from paper_2407_02490_b200.driver import PatternTable
+    from paper_2407_02490_b200.patterns import BlockSparse, VerticalSlash
+
+    model, ids = model_and_ids
+    cfgs0 = [VerticalSlash(200, 800)] * 6 + [BlockSparse(8)] * 2
+    table = PatternTable([cfgs0, [VerticalSlash(300, 1200)] * 8])
+    impl = hf.register(table)
+    seen = []
+    orig = hf.sparse_prefill_attention_forward
+
+    def spy(module, query, key, value, attention_mask, **kw):
+        out = orig(module, query, key, value, attention_mask, **kw)
+        if getattr(module, "layer_idx", 0) == 0 and not seen:
+            seen.append((query.detach().clone(), key.detach().clone(), value.detach().clone(), out[0].detach().clone()))
+        return out
+
+    from transformers import AttentionInterface
+
+    AttentionInterface.register(impl, spy)
+    try:
+        _logits(model, ids, impl)
+    finally:
+        AttentionInterface.register(impl, orig)
+    q, k, v, out = seen[0]  # [1, H, S, d] (bf16), out [1, S, H, d]
+    qn, kn, vn = (x[0].float().cpu().numpy() for x in (q, k, v))
+    got = out[0].transpose(0, 1).float().cpu().numpy()
+    hq, s, d = qn.shape
+    hkv = kn.shape[0]
+    scale = 1 / math.sqrt(d)  # = the module's scaling (head_dim ** -0.5)
+    for h, cfg in enumerate(cfgs0):
+        kvh = h // (hq // hkv)
+        if isinstance(cfg, VerticalSlash):
+            vv, ss = port.estimate_vertical_slash(qn[h], kn[kvh], cfg.k_v, cfg.k_s, cfg.last_q)
+            t, to, c, co = port.build_vs_csr(vv, ss, s, 64)
+        else:
+            t, to = port.flatten(port.block_rows_to_tiles(port.estimate_block_sparse(qn[h], kn[kvh], cfg.k_b, 64), 64))
+            c, co = np.zeros(0, np.int64), np.zeros(len(to), np.int64)
+        want = port.sparse_flash_rows(qn[h], kn[kvh], vn[kvh], scale, 64, t, to, c, co)
+        assert float(np.abs(got[h] - want).max()) < 2e-2, (h, cfg)

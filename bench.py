@@ -132,8 +132,7 @@ def run_reference_arm(args, cfg):
     value = statistics.median(vals)
     sample = (f"{info['items']} (layer, head) items per step (per pattern) of {cfg['workload']}: full estimation + "
               f"full index build, kernel on {args.ref_rows} sampled row blocks extrapolated by tiles+chips; "
-              f"kernel = {'reference _core.pyx (oracle/_ref)' if info['ref_kernel'] else 'oracle port'}; "
-              f"step latency = sum(item s)/cores")
+              f"code = {info['impl']}; step latency = sum(item s)/cores")
     line = {"impl": "reference", "modeled": True,
             "value_kind": (f"modeled: each step times a bounded sample ({info['items']} (layer, head) items; kernel on "
                            f"{args.ref_rows} row blocks each) and extrapolates to the whole workload by tile count"),
@@ -598,8 +597,7 @@ def cpu_baseline(cfg, all_cfgs):
     return {"value": round(step_s * 1e3, 3), "unit": "ms", "cores": cores,
             "kind": "reference" if info["ref_kernel"] else "port",
             "sample": f"{info['items']} (layer, head) items of {cfg['workload']} (full estimation + index, kernel on "
-                      f"16 sampled row blocks extrapolated by tiles+chips; kernel = "
-                      f"{'reference _core.pyx via oracle/_ref' if info['ref_kernel'] else 'oracle port'}); "
+                      f"16 sampled row blocks extrapolated by tiles+chips; code = {info['impl']}); "
                       f"step = sum(item s)/cores; sampled in {time.time() - t0:.1f}s wall",
             "patterns": info["patterns"]}
 

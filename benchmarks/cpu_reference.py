@@ -4,12 +4,14 @@ one place bench.py executes oracle/.
 
 One work item = one (layer, head) of the benchmark config, run exactly as the
 reference's ``run_head_timed`` does (sparse_attn.py:67-94):
-  * estimation: oracle/port.py (the numpy restatement of estimator.py:82-143);
-  * index: oracle/port.py's pure-Python Alg. 4 (vs_index.py:28-95), A-shape
-    (patterns.py:109-128) or the BS tile mapping;
-  * kernel: the reference's OWN compiled Cython kernel (_core.pyx, built from
-    /root/reference into oracle/_ref by oracle/Makefile) when present, else the
-    port -- on a row sample (other rows' lists empty), extrapolated by
+  * with the reference package installed in baseline/_ref (pip --target, see
+    DESIGN.md section 5): the reference's OWN code end to end -- its
+    estimate_vertical_slash / estimate_block_sparse, build_vs_layout / a_shape_layout,
+    and kernels.sparse_flash_attention on its compiled Cython kernel;
+  * otherwise: oracle/port.py's restatement (estimator.py:82-143, Alg. 4 of
+    vs_index.py:28-95, patterns.py:109-128) and the reference's compiled Cython
+    kernel from oracle/_ref (else the port's kernel);
+  * the kernel runs on a row sample (other rows' lists empty) and is extrapolated by
     tiles + column chips (kernel time is linear in them).
 Items run in a process pool (one process per core; the Cython kernel holds the
 GIL, so threads would not help) with OPENBLAS_NUM_THREADS=1; the step's
@@ -48,6 +50,70 @@ def g_local_np(s: int, d: int, seed: int):
     return bf16(q), bf16(k), bf16(v)
 
 
+def _timed(fn) -> float:
+    t0 = time.perf_counter()
+    fn()
+    return time.perf_counter() - t0
+
+
+def _ref_package():
+    """The reference package from baseline/_ref (None when it is not installed)."""
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.path.join(repo, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "sparseprefill")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import sparseprefill  # noqa: F401
+        from sparseprefill import estimator, kernels, patterns, sparse_attn, vs_index
+    except ImportError:
+        return None
+    if kernels.BACKEND != "cython":
+        return None
+    return estimator, kernels, patterns, sparse_attn, vs_index
+
+
+def _run_item_reference(pkg, kind, params, s, d, b, q, k, v, n_sample_rows):
+    estimator, kernels, patterns, sparse_attn, vs_index = pkg
+    t0 = time.perf_counter()
+    if kind == "vertical_slash":
+        idx = estimator.estimate_vertical_slash(q, k, patterns.VerticalSlash(*params))
+        t1 = time.perf_counter()
+        layout = vs_index.build_vs_layout(idx, s, b)
+    elif kind == "a_shape":
+        t1 = time.perf_counter()
+        layout = patterns.a_shape_layout(s, patterns.AShape(*params), b)
+    else:
+        blocks = estimator.estimate_block_sparse(q, k, patterns.BlockSparse(params[0], b))
+        t1 = time.perf_counter()
+        layout = sparse_attn.block_indices_to_layout(blocks, s, b)
+    t2 = time.perf_counter()
+    tiles, cols = layout.block_starts, layout.column_indices
+    n = len(tiles)
+    units = np.array([len(tiles[r]) + (len(cols[r]) + b - 1) // b for r in range(n)], dtype=np.int64)
+    sample = np.unique(np.linspace(0, n - 1, min(n_sample_rows, n)).round().astype(np.int64))
+    chosen = set(sample.tolist())
+    st = [list(tiles[r]) if r in chosen else [] for r in range(n)]
+    sc = [list(cols[r]) if r in chosen else [] for r in range(n)]
+    scale = 1.0 / math.sqrt(d)
+    empty = [[] for _ in range(n)]
+    # the first call in a process pays one-time allocation / first-touch costs: warm up, then
+    # time the fixed per-call cost (every row empty) and the sampled rows (best of two each)
+    kernels.sparse_flash_attention(q, k, v, scale, b, empty, empty)
+    fixed = min(_timed(lambda: kernels.sparse_flash_attention(q, k, v, scale, b, empty, empty)) for _ in range(2))
+    sampled = min(_timed(lambda: kernels.sparse_flash_attention(q, k, v, scale, b, st, sc)) for _ in range(2))
+    t4, t5 = 0.0, sampled
+    sampled_units = int(units[sample].sum())
+    total_units = int(units.sum())
+    kernel_s = fixed + max(0.0, (t5 - t4) - fixed) * total_units / max(1, sampled_units)
+    return {"kind": kind, "t_est": t1 - t0, "t_index": t2 - t1, "t_kernel": kernel_s,
+            "t_item": (t1 - t0) + (t2 - t1) + kernel_s, "units": total_units, "sampled_units": sampled_units,
+            "ref_kernel": True, "impl": "reference package (baseline/_ref): estimator, vs_index, Cython kernel"}
+
+
 def _run_item(args):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     kind, params, s, d, b, seed, n_sample_rows = args
@@ -58,8 +124,11 @@ def _run_item(args):
         sys.path.insert(0, repo)
     from oracle import port
 
-    ref = port.load_ref_core()
     q, k, v = g_local_np(s, d, seed)
+    pkg = _ref_package()
+    if pkg is not None:
+        return _run_item_reference(pkg, kind, params, s, d, b, q, k, v, n_sample_rows)
+    ref = port.load_ref_core()
     t0 = time.perf_counter()
     if kind == "vertical_slash":
         k_v, k_s, last_q = params
@@ -88,16 +157,15 @@ def _run_item(args):
     # fixed per-call cost (fp64 copies of q/k/v, output allocation): one call
     # with every row empty; only the per-row work is extrapolated.
     e_t, e_to = port.flatten([[] for _ in range(n)])
-    t3 = time.perf_counter()
     if ref is not None:
-        ref.sparse_flash_rows(q, k, v, scale, b, e_t, e_to, e_t, e_to)
-    t4 = time.perf_counter()
-    if ref is not None:
-        ref.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co)
+        ref.sparse_flash_rows(q, k, v, scale, b, e_t, e_to, e_t, e_to)  # warm-up (first-touch costs)
+        fixed = min(_timed(lambda: ref.sparse_flash_rows(q, k, v, scale, b, e_t, e_to, e_t, e_to))
+                    for _ in range(2))
+        sampled = min(_timed(lambda: ref.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co)) for _ in range(2))
     else:
-        port.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co, rows=sample)
-    t5 = time.perf_counter()
-    fixed = (t4 - t3) if ref is not None else 0.0
+        fixed = 0.0
+        sampled = _timed(lambda: port.sparse_flash_rows(q, k, v, scale, b, ts, to, cs, co, rows=sample))
+    t4, t5 = 0.0, sampled
     sampled_units = int(units[sample].sum())
     total_units = int(units.sum())
     kernel_s = fixed + max(0.0, (t5 - t4) - fixed) * total_units / max(1, sampled_units)
@@ -150,4 +218,5 @@ def run_sample(layer_cfgs, s: int, d: int, b: int, cores: int, items_per_pattern
         total += mean_item * len(heads)
     step_s = total / cores
     return step_s, {"items": len(jobs), "wall_s": wall, "patterns": per,
-                    "ref_kernel": all(r["ref_kernel"] for r in res)}
+                    "ref_kernel": all(r["ref_kernel"] for r in res),
+                    "impl": res[0].get("impl", "oracle port (estimation, merge) + oracle/_ref Cython kernel")}

@@ -19,9 +19,10 @@ from collections import OrderedDict
 
 import torch
 
+from . import kernels
 from .patterns import (AShape, BlockSparse, HeadPatternConfig, VerticalSlash, config_from_entry, config_to_entry,
                        flops_in_kernel, load_pattern_configs, save_pattern_configs)
-from .prefill import sparse_prefill_attention
+from .prefill import _pair_heads, build_layer_layout, sparse_prefill_attention
 
 
 class PatternTable:
@@ -214,6 +215,69 @@ class SparsePrefill:
             out_done[u % 2] = e2
         comp.wait_stream(d2h)
         comp.wait_stream(h2d)
+
+    def _side_stream(self, dev):
+        if getattr(self, "_est_stream", None) is None or self._est_stream.device != dev:
+            # high priority: when an SM frees up, estimation CTAs go before pending attention CTAs
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._est_stream = torch.cuda.Stream(dev, priority=hi)
+        return self._est_stream
+
+    def prefill(self, layers_qkv, outs=None, attn_events=None):
+        """Device-resident model pass through the layer pipeline.
+
+        ``layers_qkv`` = [(q, k, v)] per layer ([Hq, S, d] / [Hkv, S, d] bf16 on the device).
+        Layer l+1's estimation and index compaction run on a high-priority side stream
+        while layer l's attention runs on the current stream, so the one host read-back a
+        layer needs (the CSR totals that size its layout) waits for the side stream only
+        and never drains the attention queue; layer l's attention waits for its layout
+        through an event.  Returns the outputs (``outs`` if given), enqueued on the current
+        stream.  ``attn_events`` (optional list) receives a (start, end) CUDA event pair
+        around every layer's attention launch."""
+        layers = list(layers_qkv)
+        if len(layers) > self.table.n_layers:
+            raise ValueError(f"more layers than the pattern table holds ({self.table.n_layers})")
+        if not layers:
+            return []
+        dev = layers[0][0].device
+        comp = torch.cuda.current_stream(dev)
+        est = self._side_stream(dev)
+        est.wait_stream(comp)  # inputs produced on the current stream are visible to estimation
+        results = []
+
+        def build(layer):
+            q, k, _ = layers[layer]
+            if q.shape[0] != self.table.n_heads:
+                raise ValueError(f"layer {layer}: q has {q.shape[0]} heads, the table has {self.table.n_heads}")
+            cfgs = self.table.layer(layer)
+            b = self.table.block_size(layer, self.default_block)
+            with torch.cuda.stream(est):
+                lay = build_layer_layout(q, k, cfgs, b, stream=est, groups=self.table.device_groups(layer, dev))
+                ev = torch.cuda.Event()
+                ev.record(est)
+            return lay, ev, b
+
+        nxt = build(0)
+        for layer, (q, k, v) in enumerate(layers):
+            lay, ev, b = nxt
+            comp.wait_event(ev)
+            for t in (lay.tiles, lay.tile_offsets, lay.cols, lay.col_offsets):
+                t.record_stream(comp)  # allocated on the side stream, read by the attention
+            out = outs[layer] if outs is not None else torch.empty_like(q)
+            sc = self.scale if self.scale is not None else 1.0 / math.sqrt(q.shape[-1])
+            if attn_events is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(comp)
+            kernels.sparse_flash_attention_gpu(q, k, v, sc, b, lay.tiles, lay.tile_offsets, lay.cols, lay.col_offsets,
+                                               out=out, stream=comp,
+                                               pair_heads=_pair_heads(self.table.layer(layer), dev))
+            if attn_events is not None:
+                e1.record(comp)
+                attn_events.append((e0, e1))
+            results.append(out)
+            if layer + 1 < len(layers):
+                nxt = build(layer + 1)  # its host read-back waits for the side stream only
+        return results
 
     def __call__(self, layers_qkv, stream=None):
         """``layers_qkv``: iterable of (q, k, v) per layer, in layer order; yields outputs."""

@@ -129,3 +129,37 @@ def test_prefill_host_pipeline_matches_device_layers(P, chunks):
     torch.cuda.synchronize()
     for i in range(3):
         assert torch.equal(host_out[i], want[i]), i
+
+
+@pytest.mark.gpu
+def test_pipelined_prefill_equals_serial_layers(P):
+    """SparsePrefill.prefill (layer l+1's estimation on a side stream under layer l's
+    attention) returns exactly the serial per-layer results, also when every layer writes
+    one shared output buffer in turn (stream order) and across repeated passes."""
+    import torch
+
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(9)
+    hq, hkv, s, d = 8, 2, 4096, 128
+    table = PatternTable([[P.VerticalSlash(64, 256)] * 5 + [P.AShape(64, 512), P.BlockSparse(8), P.VerticalSlash(16, 64)],
+                          [P.AShape(128, 256)] * 4 + [P.VerticalSlash(100, 300)] * 4,
+                          [P.BlockSparse(6)] * 8,
+                          [P.VerticalSlash(200, 700)] * 8])
+    layers = [tuple(torch.randn(h, s, d, generator=g, device=dev).to(torch.bfloat16) for h in (hq, hkv, hkv))
+              for _ in range(4)]
+    model = SparsePrefill(table)
+    want = [model.layer(i, *layers[i]).clone() for i in range(4)]
+    got = model.prefill(layers)
+    torch.cuda.synchronize()
+    for i in range(4):
+        assert torch.equal(got[i], want[i]), i
+    shared = torch.empty_like(want[0])
+    events = []
+    for _ in range(3):
+        snaps = []
+        outs = model.prefill(layers, [shared] * 4, events)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[-1], want[-1])
+    assert len(events) == 12 and all(a.elapsed_time(b) > 0 for a, b in events)

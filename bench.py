@@ -250,7 +250,8 @@ def run_config(args, cfg, world, rank, local, dev, with_cpu, with_e2e, steps, la
     from paper_2407_02490_b200 import _lib, kernels
     from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
     from paper_2407_02490_b200.prefill import _pair_heads
-    from paper_2407_02490_b200.sharding import gather_heads, max_over_ranks, plan_heads_lpt, shard_heads
+    from paper_2407_02490_b200.sharding import (gather_heads, gather_heads_async, max_over_ranks, plan_heads_lpt,
+                                                shard_heads)
 
     S, HQ, HKV, L, D, B = cfg["seq_len"], cfg["hq"], cfg["hkv"], cfg["layers"], 128, 64
     all_cfgs = layer_configs(cfg)[:L]
@@ -291,9 +292,19 @@ def run_config(args, cfg, world, rank, local, dev, with_cpu, with_e2e, steps, la
         if not args.serial:
             # the public model pass: layer l+1's estimation + compaction on a side stream
             # under layer l's attention (SparsePrefill.prefill)
-            model.prefill(layers_qkv, outs, attn_events if record else None)
-            if args.gather and world > 1:
-                gather_heads(out, shards)
+            pending = []
+
+            def after_layer(layer, o):
+                # the optional output all-gather, overlapped with the next layers' compute
+                # (at most two exchanges in flight)
+                pending.append(gather_heads_async(o, shards))
+                if len(pending) > 2:
+                    pending.pop(0).wait()
+
+            model.prefill(layers_qkv, outs, attn_events if record else None,
+                          after_layer if (args.gather and world > 1) else None)
+            for pg in pending:
+                pg.wait()
             return
         for layer in range(L):
             if record:

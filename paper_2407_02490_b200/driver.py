@@ -223,7 +223,7 @@ class SparsePrefill:
             self._est_stream = torch.cuda.Stream(dev, priority=hi)
         return self._est_stream
 
-    def prefill(self, layers_qkv, outs=None, attn_events=None):
+    def prefill(self, layers_qkv, outs=None, attn_events=None, after_layer=None):
         """Device-resident model pass through the layer pipeline.
 
         ``layers_qkv`` = [(q, k, v)] per layer ([Hq, S, d] / [Hkv, S, d] bf16 on the device).
@@ -233,7 +233,9 @@ class SparsePrefill:
         and never drains the attention queue; layer l's attention waits for its layout
         through an event.  Returns the outputs (``outs`` if given), enqueued on the current
         stream.  ``attn_events`` (optional list) receives a (start, end) CUDA event pair
-        around every layer's attention launch."""
+        around every layer's attention launch; ``after_layer(layer, out)`` (optional) is
+        called once the layer's attention is enqueued (e.g. to start its output all-gather
+        while the next layer computes, sharding.gather_heads_async)."""
         layers = list(layers_qkv)
         if len(layers) > self.table.n_layers:
             raise ValueError(f"more layers than the pattern table holds ({self.table.n_layers})")
@@ -275,6 +277,8 @@ class SparsePrefill:
                 e1.record(comp)
                 attn_events.append((e0, e1))
             results.append(out)
+            if after_layer is not None:
+                after_layer(layer, out)
             if layer + 1 < len(layers):
                 nxt = build(layer + 1)  # its host read-back waits for the side stream only
         return results

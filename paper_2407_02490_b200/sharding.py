@@ -152,8 +152,30 @@ def plan_heads_lpt(head_costs, n_kv_heads: int, world: int, rank: int) -> HeadSh
     return HeadShard(rank, world, heads, qpk)
 
 
-def gather_heads(local: torch.Tensor, shards, group=None) -> torch.Tensor:
-    """All-gather per-rank [n_q_local, ...] blocks into [n_q_total, ...] (global head order)."""
+class PendingGather:
+    """An in-flight all-gather of per-rank head blocks (gather_heads_async)."""
+
+    def __init__(self, work, bufs, shards, like: torch.Tensor):
+        self._work, self._bufs, self._shards, self._like = work, bufs, shards, like
+
+    def wait(self) -> torch.Tensor:
+        """Make the current stream wait for the exchange; the full [n_q_total, ...] tensor."""
+        self._work.wait()
+        bufs, shards, local = self._bufs, self._shards, self._like
+        sizes = [s.n_q for s in shards]
+        if all(s.contiguous for s in shards) and [s.q_begin for s in shards] == sorted(s.q_begin for s in shards):
+            return torch.cat([b[:n] for b, n in zip(bufs, sizes)], dim=0)
+        full = torch.empty((sum(sizes),) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        for b, s in zip(bufs, shards):
+            full[torch.tensor(s.q_heads, device=local.device)] = b[: s.n_q]
+        return full
+
+
+def gather_heads_async(local: torch.Tensor, shards, group=None) -> PendingGather:
+    """Start the all-gather of this rank's [n_q_local, ...] block (SURVEY.md 8(e)'s optional
+    collective) without blocking: the block is first copied into a padded send buffer on
+    the current stream, so the caller may overwrite ``local`` right away (e.g. with the
+    next layer's attention) while the exchange overlaps it; ``wait()`` assembles."""
     import torch.distributed as dist
 
     sizes = [s.n_q for s in shards]
@@ -161,14 +183,13 @@ def gather_heads(local: torch.Tensor, shards, group=None) -> torch.Tensor:
     pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
     bufs = [torch.empty_like(pad) for _ in shards]
-    dist.all_gather(bufs, pad, group=group)
-    if all(s.contiguous for s in shards) and [s.q_begin for s in shards] == sorted(s.q_begin for s in shards):
-        return torch.cat([b[:n] for b, n in zip(bufs, sizes)], dim=0)
-    total = sum(sizes)
-    full = torch.empty((total,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    for b, s in zip(bufs, shards):
-        full[torch.tensor(s.q_heads, device=local.device)] = b[: s.n_q]
-    return full
+    work = dist.all_gather(bufs, pad, group=group, async_op=True)
+    return PendingGather(work, bufs, shards, local)
+
+
+def gather_heads(local: torch.Tensor, shards, group=None) -> torch.Tensor:
+    """All-gather per-rank [n_q_local, ...] blocks into [n_q_total, ...] (global head order)."""
+    return gather_heads_async(local, shards, group).wait()
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:

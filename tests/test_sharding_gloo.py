@@ -83,7 +83,7 @@ def _worker(rank, world, port, result, plan):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import port as orc
-        from paper_2407_02490_b200.sharding import gather_heads, max_over_ranks
+        from paper_2407_02490_b200.sharding import gather_heads, gather_heads_async, max_over_ranks
 
         s_len, d, b, hq, hkv = 96, 16, 16, 6, 2
         rng = np.random.Generator(np.random.PCG64(3))
@@ -107,6 +107,11 @@ def _worker(rank, world, port, result, plan):
             kv = me.local_kv_index(h)
             outs.append(orc.sparse_flash_rows(q[h], k_loc[kv], v_loc[kv], d ** -0.5, b, ts, to, cs, co))
         full = gather_heads(torch.from_numpy(np.stack(outs)), shards)
+        # overlapped form: the block may be overwritten (next layer) right after the call
+        loc = torch.from_numpy(np.stack(outs)).clone()
+        pending = gather_heads_async(loc, shards)
+        loc.fill_(float("nan"))
+        full_async = pending.wait()
         t = max_over_ranks(float(rank + 1))
         if rank == 0:
             ref = []
@@ -118,6 +123,7 @@ def _worker(rank, world, port, result, plan):
                 ref.append(orc.sparse_flash_rows(q[h], k[h // (hq // hkv)], v[h // (hq // hkv)], d ** -0.5, b,
                                                  ts, to, cs, co))
             result["max_err"] = float(np.max(np.abs(full.numpy() - np.stack(ref))))
+            result["async_equal"] = bool(torch.equal(full_async, full))
             result["shape"] = tuple(full.shape)
             result["t"] = t
     finally:
@@ -131,6 +137,7 @@ def test_two_rank_gloo_sharded_layer(world, plan):
     mp.spawn(_worker, args=(world, _free_port(), result, plan), nprocs=world, join=True)
     assert result["shape"] == (6, 96, 16)
     assert result["max_err"] == 0.0  # same CPU computation, reassembled in head order
+    assert result["async_equal"]  # the overlapped gather copies the block before returning
     assert result["t"] == float(world)  # max over ranks
 
 

@@ -571,15 +571,19 @@ __global__ void __launch_bounds__(kFbThreads, 1) vs_fb_kernel(const __nv_bfloat1
           }
       }
       __syncthreads();
+      // columns on warps 0-1, diagonals on warps 2-5 (concurrently); each sum runs over the
+      // rows in ascending order (the reference's order), its loads issued ahead of the adds
       if (tid < 64) {
         double cs = 0.0;
+#pragma unroll 16
         for (int ii = 0; ii < 64; ++ii) cs += (double)Ps[ii][tid];
         if (k0 + tid < S) a.vscore[(int64_t)h * S + k0 + tid] = cs;
-      }
-      // diagonal cl = key - row in [-63, 63]; offset o = (S - 64 + row) - (k0 + key)
-      for (int cl = tid - 63; cl <= 63; cl += kFbThreads) {
+      } else if (tid < 64 + 127) {
+        // diagonal cl = key - row in [-63, 63]; offset o = (S - 64 + row) - (k0 + key)
+        const int cl = tid - 64 - 63;
         const int ii0 = max(0, -cl), ii1 = min(64, 64 - cl);
         double ds = 0.0;
+#pragma unroll 16
         for (int ii = ii0; ii < ii1; ++ii) ds += (double)Ps[ii][ii + cl];
         const int o = S - 64 - k0 - cl;
         if (o >= 0 && o < S && ds != 0.0) atomicAdd(a.sscore + (int64_t)h * S + o, ds);

@@ -11,7 +11,7 @@
 //    entries themselves are written by the BS estimator (estimate_bs.cu).
 //  * layout_area, patterns.py:147-184 (diagonal tile clipped to its lower
 //    triangle, column chips rounded up to B).
-#include <cub/device/device_scan.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "spf.h"
 #include "spf_internal.h"
@@ -254,6 +254,50 @@ dim3 merge_grid(int S, int B, int n_heads, int rpc) {
   return dim3((unsigned)((n_rows + rpc - 1) / rpc), (unsigned)n_heads);
 }
 
+// CSR offsets: a two-level inclusive scan of the int64 row counts (tiles of kScanTile rows:
+// per-tile sums, one CTA scanning the tile sums, per-tile scans plus the tile's prefix).
+constexpr int kScanThreads = 1024, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+using ScanBlock = cub::BlockScan<int64_t, kScanThreads>;
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int64_t* __restrict__ counts, int64_t n,
+                                                                   int64_t* __restrict__ block_sums) {
+  __shared__ typename ScanBlock::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t x = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) x += base + i < n ? counts[base + i] : 0;
+  int64_t incl, total;
+  ScanBlock(tmp).InclusiveSum(x, incl, total);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_blocks_kernel(int64_t* __restrict__ block_sums, int64_t nb) {
+  __shared__ typename ScanBlock::TempStorage tmp;
+  int64_t x[kScanItems];
+  const int64_t base = (int64_t)threadIdx.x * kScanItems;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) x[i] = base + i < nb ? block_sums[base + i] : 0;
+  ScanBlock(tmp).ExclusiveSum(x, x);  // block_sums[b] <- prefix of the tiles before b
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < nb) block_sums[base + i] = x[i];
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int64_t* __restrict__ counts, int64_t n,
+                                                                  const int64_t* __restrict__ block_prefix,
+                                                                  int64_t* __restrict__ out) {
+  __shared__ typename ScanBlock::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t x[kScanItems];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) x[i] = base + i < n ? counts[base + i] : 0;
+  ScanBlock(tmp).InclusiveSum(x, x);
+  const int64_t pre = block_prefix[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) out[base + i] = x[i] + pre;
+}
+
 dim3 row_grid(int S, int B, int n_heads) { return dim3((unsigned)(((S + B - 1) / B + kThreads - 1) / kThreads), (unsigned)n_heads); }
 
 }  // namespace
@@ -264,9 +308,8 @@ using namespace spf;
 extern "C" {
 
 size_t spf_scan_workspace_size(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n);
-  return bytes + 256;
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  return (size_t)(nb + 1) * sizeof(int64_t) + 256;
 }
 
 int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t* total_host, void* workspace,
@@ -275,13 +318,17 @@ int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t*
   int rc;
   if ((rc = check_cuda(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st), "csr offsets memset"))) return rc;
   if (n > 0) {
-    size_t bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, bytes, counts, offsets + 1, n);
-    if (workspace == nullptr || workspace_bytes < bytes)
-      return set_error(SPF_ERR_INVALID, "scan workspace too small (%zu < %zu)", workspace_bytes, bytes);
-    note_launches(2);
-    if ((rc = check_cuda(cub::DeviceScan::InclusiveSum(workspace, bytes, counts, offsets + 1, n, st), "csr scan")))
-      return rc;
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb > kScanTile) return set_error(SPF_ERR_INVALID, "scan of %lld rows exceeds the two-level limit", (long long)n);
+    if (workspace == nullptr || workspace_bytes < spf_scan_workspace_size(n))
+      return set_error(SPF_ERR_INVALID, "scan workspace too small (%zu < %zu)", workspace_bytes,
+                       spf_scan_workspace_size(n));
+    int64_t* block_sums = reinterpret_cast<int64_t*>(workspace);
+    note_launches(3);
+    scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(counts, n, block_sums);
+    scan_blocks_kernel<<<1, kScanThreads, 0, st>>>(block_sums, nb);
+    scan_apply_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(counts, n, block_sums, offsets + 1);
+    if ((rc = check_cuda(cudaGetLastError(), "csr scan"))) return rc;
   }
   if (total_host != nullptr) {
     if ((rc = check_cuda(cudaMemcpyAsync(total_host, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st),

@@ -7,12 +7,14 @@ Drop-in mirror of /root/reference/pkg/src/sparseprefill/estimator.py:
 * ``argtopk`` (59-67): stable descending order, ties to the lower index;
 * ``estimate_vertical_slash(q, k, cfg)`` (82-114) and
   ``estimate_block_sparse(q, k, cfg)`` (117-143) take NumPy [S, d] arrays
-  like the reference (fp32) and run libspf's fp64 estimation kernels
-  (spf_vs_estimate mode SPF_VS_EXACT / spf_bs_estimate), so the selected
-  index sets are those of the reference.  bf16 device tensors (the production
-  path) use the tensor-core VS estimator whose selections are certified per
-  head against its error model; uncertified heads are re-run on the fp64
-  path.
+  like the reference (fp32).  They call the production entry (mode "fast"),
+  whose tensor-core path takes bf16 inputs only, so fp32 inputs run libspf's
+  fp64 estimation kernels (the SPF_VS_EXACT path / spf_bs_estimate) and the
+  selected index sets are the reference's.  bf16 device tensors (the
+  production path) score on the tensor cores; a head's selection is kept only
+  when a rigorous bound on the score error separates its top-k boundary
+  (estimate_vs_tc.cu), otherwise the head is re-run on the fp64 path in the
+  same call -- the sets equal the fp64 path's either way.
 
 ``estimate_vertical_slash_gpu`` / ``estimate_block_sparse_gpu`` are the
 batched multi-head (GQA) device entries used by ``prefill.py``.

@@ -289,38 +289,22 @@ def run_config(args, cfg, world, rank, local, dev, with_cpu, with_e2e, steps, la
     outs = [out] * L  # every layer writes the same buffer (stream-ordered)
 
     def step(record=False):
-        if args.pipeline:
-            # the public model pass: layer l+1's estimation + compaction on a side stream
-            # under layer l's attention (SparsePrefill.prefill)
-            pending = []
+        # the public model pass (SparsePrefill.prefill): per layer estimation, compaction into the
+        # speculatively sized CSR (checked on the device; one read-back per step) and the attention
+        # launch; --pipeline overlaps layer l+1's estimation with layer l's attention instead
+        pending = []
 
-            def after_layer(layer, o):
-                # the optional output all-gather, overlapped with the next layers' compute
-                # (at most two exchanges in flight)
-                pending.append(gather_heads_async(o, shards))
-                if len(pending) > 2:
-                    pending.pop(0).wait()
+        def after_layer(layer, o):
+            # the optional output all-gather, overlapped with the next layers' compute
+            # (at most two exchanges in flight)
+            pending.append(gather_heads_async(o, shards))
+            if len(pending) > 2:
+                pending.pop(0).wait()
 
-            model.prefill(layers_qkv, outs, attn_events if record else None,
-                          after_layer if (args.gather and world > 1) else None)
-            for pg in pending:
-                pg.wait()
-            return
-        for layer in range(L):
-            if record:
-                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-                e0.record(stream)
-            lay = P.build_layer_layout(Q[layer], K[layer], cfgs[layer], B, groups=table.device_groups(layer, dev))
-            if record:
-                e1.record(stream)
-            kernels.sparse_flash_attention_gpu(Q[layer], K[layer], V[layer], scale, B, lay.tiles, lay.tile_offsets,
-                                               lay.cols, lay.col_offsets, out=out, pair_heads=pair_masks[layer])
-            if record:
-                e2.record(stream)
-                est_events.append((e0, e1))
-                attn_events.append((e1, e2))
-            if args.gather and world > 1:
-                gather_heads(out, shards)
+        model.prefill(layers_qkv, outs, attn_events if record else None,
+                      after_layer if (args.gather and world > 1) else None, pipeline=args.pipeline)
+        for pg in pending:
+            pg.wait()
 
     # ---- warm-up + layout statistics (deterministic inputs -> fixed layouts) ----
     step()
@@ -462,9 +446,10 @@ def run_config(args, cfg, world, rank, local, dev, with_cpu, with_e2e, steps, la
         "attention_ms_per_step": round(attn_step_ms, 3),
         "estimate_index_ms_per_step": round(est_step_ms, 3),
         "estimate_index_exposed_ms_per_step": round(ms_per_step - attn_step_ms, 3),
-        "layer_pipeline": ("SparsePrefill.prefill: layer l+1 estimation + compaction on a high-priority side stream "
-                           "under layer l's attention") if args.pipeline else "serial: per layer estimation + "
-                           "compaction, then the attention launch, one stream",
+        "layer_pipeline": ("SparsePrefill.prefill(pipeline=True): layer l+1 estimation + compaction on a "
+                           "high-priority side stream under layer l's attention") if args.pipeline else
+                          ("SparsePrefill.prefill: one stream, CSR sized from the previous step and checked on the "
+                           "device (spf_csr_guard), one host read-back per step"),
         "dense_baseline": dense,
     }
     del Q, K, V, out
@@ -486,10 +471,10 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the 1M Vertical-Slash sub-record of the C2 line")
     ap.add_argument("--pipeline", action="store_true",
-                    help="time the pipelined model pass (SparsePrefill.prefill: layer l+1's estimation under layer l's "
-                         "attention on a side stream); measured equal to the serial step on C2 (494.3 vs 494.7 ms), "
-                         "but the attention launches then absorb the estimation kernels' SM time, so the default "
-                         "serial step keeps the kernel roofline clean")
+                    help="time the pipelined model pass (layer l+1's estimation under layer l's attention on a side "
+                         "stream); measured equal to the serial step on C2 (494.3 vs 494.7 ms), but the attention "
+                         "launches then absorb the estimation kernels' SM time, so the default one-stream pass keeps "
+                         "the kernel roofline clean")
     ap.add_argument("--dry-run", action="store_true", help="CPU plumbing check of the rank launch (gloo, no GPU)")
     ap.add_argument("--e2e-chunks", type=int, default=0,
                     help="head chunks (whole kv groups) per layer in the host-buffer pipeline of the e2e leg; "

@@ -174,6 +174,15 @@ size_t spf_scan_workspace_size(int64_t n);
  * *total_host (synchronising `stream`) when total_host != NULL. */
 int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t* total_host, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* Speculative sizing without a host read-back: if tile_offsets[n] > cap_tiles or
+ * col_offsets[n] > cap_cols, both offset arrays are zeroed (every row empty: the
+ * fills write nothing and the attention produces zero rows, so no buffer of the
+ * given capacities is overrun) and *overflow = 1; totals[0..1] receive the two
+ * true totals either way.  The caller reads the flag later and redoes the layer
+ * with an exact size.  Stream-ordered, no host sync.  (Replaces the size
+ * read-back that kernels.py:28-35's host-side flattening implies.) */
+int spf_csr_guard(int64_t* tile_offsets, int64_t* col_offsets, int64_t n, int64_t cap_tiles, int64_t cap_cols,
+                  int32_t* overflow, int64_t* totals, void* stream);
 
 /* Vertical-Slash point-range merge, vs_index.py:28-95 (Alg. 4), bit-exact.
  * vertical [n_heads][n_v] ascending, slash [n_heads][n_s] descending. */

@@ -47,6 +47,7 @@ SIGNATURES = {
                                  _vp, _vp, _vp, _c_size, _vp]),
     "spf_scan_workspace_size": (_c_size, [_i64]),
     "spf_csr_offsets": (_c_int, [_vp, _i64, _vp, _vp, _vp, _c_size, _vp]),
+    "spf_csr_guard": (_c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "spf_vs_layout_count": (_c_int, [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "spf_vs_layout_fill": (_c_int, [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
                                     _vp]),

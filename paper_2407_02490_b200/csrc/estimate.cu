@@ -288,6 +288,8 @@ __global__ void __launch_bounds__(kBsThreads) bs_row_kernel(double* __restrict__
   for (int b = tid; b < n; b += kBsThreads) pv[b] = __double2float_rn(sr[b] / l);
   __syncthreads();
   const int64_t row = (int64_t)h * N + r;
+  // a row emptied by spf_csr_guard (speculative sizing overflowed) receives nothing
+  if (tile_offsets[row + 1] - tile_offsets[row] < min(k_b, n)) return;
   TK::run(sm, pv, n, min(k_b, n), r, false, tile_starts + tile_offsets[row], B);
 }
 

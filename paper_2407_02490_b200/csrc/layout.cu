@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
   for (int r = blockIdx.x * rows_per_cta + warp; r < r_end; r += kMergeWarps) {
     const int64_t row = (int64_t)h * n_rows + r;
     const int q_start = r * B, q_end = min(q_start + B, S);
+    // a row emptied by spf_csr_guard (both counts 0) receives nothing (warp-uniform)
+    if (kFill && tile_off[row + 1] == tile_off[row] && col_off[row + 1] == col_off[row]) continue;
     int32_t* tout = kFill ? tiles + tile_off[row] : nullptr;
     int32_t* cout = kFill ? cols + col_off[row] : nullptr;
     int64_t nt = 0, nc = 0;
@@ -198,6 +200,7 @@ __global__ void ashape_kernel(const int32_t* __restrict__ head_ids, int S, int B
     cnt[row] = sink_n + local_n;
     return;
   }
+  if (off[row + 1] - off[row] < sink_n + local_n) return;  // row emptied by spf_csr_guard
   int32_t* out = tiles + off[row];
   for (int j = 0; j < sink_n; ++j) out[j] = j * B;
   for (int j = 0; j < local_n; ++j) out[sink_n + j] = local_start + j * B;
@@ -298,6 +301,27 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int64_t*
     if (base + i < n) out[base + i] = x[i] + pre;
 }
 
+// spf_csr_guard: one CTA; thread 0 compares the totals with the capacities, then on overflow
+// every thread helps zero the two offset arrays.
+__global__ void __launch_bounds__(1024) csr_guard_kernel(int64_t* __restrict__ toff, int64_t* __restrict__ coff,
+                                                         int64_t n, int64_t cap_t, int64_t cap_c,
+                                                         int32_t* __restrict__ overflow, int64_t* __restrict__ totals) {
+  __shared__ int over;
+  if (threadIdx.x == 0) {
+    const int64_t t = toff[n], c = coff[n];
+    totals[0] = t;
+    totals[1] = c;
+    over = (t > cap_t || c > cap_c) ? 1 : 0;
+    if (over) *overflow = 1;
+  }
+  __syncthreads();
+  if (!over) return;
+  for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) {
+    toff[i] = 0;
+    coff[i] = 0;
+  }
+}
+
 dim3 row_grid(int S, int B, int n_heads) { return dim3((unsigned)(((S + B - 1) / B + kThreads - 1) / kThreads), (unsigned)n_heads); }
 
 }  // namespace
@@ -337,6 +361,16 @@ int spf_csr_offsets(const int64_t* counts, int64_t n, int64_t* offsets, int64_t*
     if ((rc = check_cuda(cudaStreamSynchronize(st), "csr total sync"))) return rc;
   }
   return SPF_OK;
+}
+
+int spf_csr_guard(int64_t* tile_offsets, int64_t* col_offsets, int64_t n, int64_t cap_tiles, int64_t cap_cols,
+                  int32_t* overflow, int64_t* totals, void* stream) {
+  if (n < 0 || cap_tiles < 0 || cap_cols < 0) return set_error(SPF_ERR_INVALID, "negative size or capacity");
+  if (!tile_offsets || !col_offsets || !overflow || !totals) return set_error(SPF_ERR_INVALID, "null pointer");
+  note_launches(1);
+  csr_guard_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(tile_offsets, col_offsets, n, cap_tiles,
+                                                                           cap_cols, overflow, totals);
+  return check_cuda(cudaGetLastError(), "csr guard");
 }
 
 int spf_vs_layout_count(const int32_t* vertical, int n_v, const int32_t* slash, int n_s, const int32_t* head_ids,

@@ -22,7 +22,7 @@ import torch
 from . import kernels
 from .patterns import (AShape, BlockSparse, HeadPatternConfig, VerticalSlash, config_from_entry, config_to_entry,
                        flops_in_kernel, load_pattern_configs, save_pattern_configs)
-from .prefill import _pair_heads, build_layer_layout, sparse_prefill_attention
+from .prefill import _pair_heads, build_layer_layout, build_layer_layout_into, sparse_prefill_attention
 
 
 class PatternTable:
@@ -223,24 +223,106 @@ class SparsePrefill:
             self._est_stream = torch.cuda.Stream(dev, priority=hi)
         return self._est_stream
 
-    def prefill(self, layers_qkv, outs=None, attn_events=None, after_layer=None):
-        """Device-resident model pass through the layer pipeline.
+    def prefill(self, layers_qkv, outs=None, attn_events=None, after_layer=None, pipeline: bool = False):
+        """Device-resident model pass: ``layers_qkv`` = [(q, k, v)] per layer ([Hq, S, d] /
+        [Hkv, S, d] bf16 on the device); returns the outputs (``outs`` if given), enqueued on
+        the current stream.  ``attn_events`` (optional list) receives a (start, end) CUDA event
+        pair around every layer's attention launch; ``after_layer(layer, out)`` (optional) is
+        called once a layer's attention is enqueued (e.g. to start its output all-gather while
+        the next layer computes, sharding.gather_heads_async).
 
-        ``layers_qkv`` = [(q, k, v)] per layer ([Hq, S, d] / [Hkv, S, d] bf16 on the device).
-        Layer l+1's estimation and index compaction run on a high-priority side stream
-        while layer l's attention runs on the current stream, so the one host read-back a
-        layer needs (the CSR totals that size its layout) waits for the side stream only
-        and never drains the attention queue; layer l's attention waits for its layout
-        through an event.  Returns the outputs (``outs`` if given), enqueued on the current
-        stream.  ``attn_events`` (optional list) receives a (start, end) CUDA event pair
-        around every layer's attention launch; ``after_layer(layer, out)`` (optional) is
-        called once the layer's attention is enqueued (e.g. to start its output all-gather
-        while the next layer computes, sharding.gather_heads_async)."""
+        Default (``pipeline=False``): one stream and no per-layer host sync.  A layer's CSR
+        is sized from what the same layer needed on the previous call (+12.5 %), in one
+        grow-only buffer pair shared by the layers; ``spf_csr_guard`` checks the sizes on the
+        device and empties an overflowing layer instead of overrunning anything.  One
+        read-back per call checks the flags and recomputes an overflowed layer with an exact
+        size (calling ``after_layer`` again for it).  A layer seen for the first time is
+        sized exactly (one host read-back).
+
+        ``pipeline=True``: layer l+1's estimation and compaction run on a high-priority side
+        stream while layer l's attention runs (exact sizing; the read-back waits for the
+        side stream only)."""
         layers = list(layers_qkv)
         if len(layers) > self.table.n_layers:
             raise ValueError(f"more layers than the pattern table holds ({self.table.n_layers})")
         if not layers:
             return []
+        for layer, (q, _, _) in enumerate(layers):
+            if q.shape[0] != self.table.n_heads:
+                raise ValueError(f"layer {layer}: q has {q.shape[0]} heads, the table has {self.table.n_heads}")
+        if pipeline:
+            return self._prefill_pipelined(layers, outs, attn_events, after_layer)
+        return self._prefill_speculative(layers, outs, attn_events, after_layer)
+
+    def _attend(self, layer, q, k, v, lay, b, out, stream, attn_events):
+        sc = self.scale if self.scale is not None else 1.0 / math.sqrt(q.shape[-1])
+        if attn_events is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        kernels.sparse_flash_attention_gpu(q, k, v, sc, b, lay.tiles, lay.tile_offsets, lay.cols, lay.col_offsets,
+                                           out=out, stream=stream, pair_heads=_pair_heads(self.table.layer(layer),
+                                                                                          q.device))
+        if attn_events is not None:
+            e1.record(stream)
+            attn_events.append((e0, e1))
+
+    def _prefill_speculative(self, layers, outs, attn_events, after_layer):
+        dev = layers[0][0].device
+        comp = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_caps"):
+            self._caps = {}
+        n_layers = len(layers)
+        flags = torch.zeros(n_layers, dtype=torch.int32, device=dev)
+        totals = torch.zeros((n_layers, 2), dtype=torch.int64, device=dev)
+        keys = [(layer, tuple(q.shape), tuple(k.shape), str(dev)) for layer, (q, k, _) in enumerate(layers)]
+
+        def arena(nt, nc):
+            cur = getattr(self, "_arena", None)
+            if cur is None or cur[0].device != dev or cur[0].numel() < nt or cur[1].numel() < nc:
+                nt2 = max(nt, cur[0].numel() if cur is not None and cur[0].device == dev else 0)
+                nc2 = max(nc, cur[1].numel() if cur is not None and cur[1].device == dev else 0)
+                self._arena = (torch.empty(max(nt2, 1), dtype=torch.int32, device=dev),
+                               torch.empty(max(nc2, 1), dtype=torch.int32, device=dev))
+            return self._arena
+
+        speculated = []
+        results = []
+        for layer, (q, k, v) in enumerate(layers):
+            cfgs = self.table.layer(layer)
+            b = self.table.block_size(layer, self.default_block)
+            groups = self.table.device_groups(layer, dev)
+            out = outs[layer] if outs is not None else torch.empty_like(q)
+            cap = self._caps.get(keys[layer])
+            if cap is None:
+                lay = build_layer_layout(q, k, cfgs, b, groups=groups)
+                self._caps[keys[layer]] = (lay.n_tiles + lay.n_tiles // 8 + 64, lay.n_cols + lay.n_cols // 8 + 64)
+            else:
+                t_buf, c_buf = arena(*cap)
+                lay = build_layer_layout_into(q, k, cfgs, b, t_buf[:cap[0]], c_buf[:cap[1]], flags[layer:layer + 1],
+                                              totals[layer], groups=groups)
+                speculated.append(layer)
+            self._attend(layer, q, k, v, lay, b, out, comp, attn_events)
+            results.append(out)
+            if after_layer is not None:
+                after_layer(layer, out)
+        if speculated:
+            f = flags.cpu()  # the one read-back of the call
+            if int(f.sum()):
+                tot = totals.cpu()
+                for layer in speculated:
+                    if int(f[layer]):
+                        q, k, v = layers[layer]
+                        nt, nc = int(tot[layer, 0]), int(tot[layer, 1])
+                        self._caps[keys[layer]] = (nt + nt // 8 + 64, nc + nc // 8 + 64)
+                        b = self.table.block_size(layer, self.default_block)
+                        lay = build_layer_layout(q, k, self.table.layer(layer), b,
+                                                 groups=self.table.device_groups(layer, dev))
+                        self._attend(layer, q, k, v, lay, b, results[layer], comp, None)
+                        if after_layer is not None:
+                            after_layer(layer, results[layer])
+        return results
+
+    def _prefill_pipelined(self, layers, outs, attn_events, after_layer):
         dev = layers[0][0].device
         comp = torch.cuda.current_stream(dev)
         est = self._side_stream(dev)
@@ -249,8 +331,6 @@ class SparsePrefill:
 
         def build(layer):
             q, k, _ = layers[layer]
-            if q.shape[0] != self.table.n_heads:
-                raise ValueError(f"layer {layer}: q has {q.shape[0]} heads, the table has {self.table.n_heads}")
             cfgs = self.table.layer(layer)
             b = self.table.block_size(layer, self.default_block)
             with torch.cuda.stream(est):
@@ -266,16 +346,7 @@ class SparsePrefill:
             for t in (lay.tiles, lay.tile_offsets, lay.cols, lay.col_offsets):
                 t.record_stream(comp)  # allocated on the side stream, read by the attention
             out = outs[layer] if outs is not None else torch.empty_like(q)
-            sc = self.scale if self.scale is not None else 1.0 / math.sqrt(q.shape[-1])
-            if attn_events is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(comp)
-            kernels.sparse_flash_attention_gpu(q, k, v, sc, b, lay.tiles, lay.tile_offsets, lay.cols, lay.col_offsets,
-                                               out=out, stream=comp,
-                                               pair_heads=_pair_heads(self.table.layer(layer), dev))
-            if attn_events is not None:
-                e1.record(comp)
-                attn_events.append((e0, e1))
+            self._attend(layer, q, k, v, lay, b, out, comp, attn_events)
             results.append(out)
             if after_layer is not None:
                 after_layer(layer, out)

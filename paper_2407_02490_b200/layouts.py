@@ -36,6 +36,15 @@ def csr_offsets(counts: torch.Tensor, stream=None, want_total: bool = True):
     return offsets, (int(total[0]) if want_total else None)
 
 
+def csr_guard(tile_offsets: torch.Tensor, col_offsets: torch.Tensor, cap_tiles: int, cap_cols: int,
+              overflow: torch.Tensor, totals: torch.Tensor, stream=None):
+    """spf_csr_guard: speculative CSR sizing checked on the device (see prefill.build_layer_layout_into)."""
+    lib = _lib.load()
+    _lib.check(lib.spf_csr_guard(_dev.ptr(tile_offsets), _dev.ptr(col_offsets), tile_offsets.numel() - 1,
+                                 int(cap_tiles), int(cap_cols), _dev.ptr(overflow), _dev.ptr(totals),
+                                 _dev.stream_handle(stream)), "spf_csr_guard")
+
+
 def vs_count(vertical: torch.Tensor, slash: torch.Tensor, head_ids, seq_len: int, block_size: int,
              tile_counts: torch.Tensor, col_counts: torch.Tensor, stream=None):
     lib = _lib.load()

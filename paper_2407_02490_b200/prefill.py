@@ -90,7 +90,8 @@ def build_layer_layout(q: torch.Tensor, k: torch.Tensor, head_cfgs, block_size: 
     return _build_layer_layout(q, k, head_cfgs, block_size, None, groups)
 
 
-def _build_layer_layout(q, k, head_cfgs, block_size, stream, groups) -> LayerLayout:
+def _layout_counts(q, k, head_cfgs, block_size, stream, groups):
+    """Estimation + per-row counts + the two CSR scans (device only, no host sync)."""
     dev = _dev.require_cuda(q.device)
     hq, s_len, _ = q.shape
     if len(head_cfgs) != hq:
@@ -99,9 +100,9 @@ def _build_layer_layout(q, k, head_cfgs, block_size, stream, groups) -> LayerLay
         if isinstance(cfg, BlockSparse) and cfg.block_size != block_size:
             raise ValueError("all heads of a layer must share one block size "
                              f"(BlockSparse block_size {cfg.block_size} != {block_size})")
-    n = n_block_rows(s_len, block_size)
     if groups is None:
         groups = _group_heads(head_cfgs, dev)
+    n = n_block_rows(s_len, block_size)
     tc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
     cc = torch.zeros(hq * n, dtype=torch.int64, device=dev)
     vs_sel = {}
@@ -116,19 +117,49 @@ def _build_layer_layout(q, k, head_cfgs, block_size, stream, groups) -> LayerLay
             layouts.bs_count(ids, m, s_len, block_size, cfg.k_b, tc, stream)
     toff, _ = layouts.csr_offsets(tc, stream, want_total=False)
     coff, _ = layouts.csr_offsets(cc, stream, want_total=False)
-    totals = torch.stack([toff[-1], coff[-1]]).cpu()  # the one host sync of the layer
+    return dict(groups=groups, vs_sel=vs_sel, toff=toff, coff=coff, s_len=s_len, hq=hq)
+
+
+def _layout_fill(q, k, ctx, block_size, tiles, cols, stream):
+    s_len = ctx["s_len"]
+    for cfg, ids, m in ctx["groups"]:
+        if isinstance(cfg, VerticalSlash):
+            vert, sl = ctx["vs_sel"][cfg]
+            layouts.vs_fill(vert, sl, ids, s_len, block_size, ctx["toff"], ctx["coff"], tiles, cols, stream)
+        elif isinstance(cfg, AShape):
+            layouts.ashape_fill(ids, m, s_len, block_size, cfg, ctx["toff"], tiles, stream)
+        else:
+            estimate_block_sparse_gpu(q, k, cfg, ids, ctx["toff"], tiles, stream)
+
+
+def _build_layer_layout(q, k, head_cfgs, block_size, stream, groups) -> LayerLayout:
+    dev = _dev.require_cuda(q.device)
+    ctx = _layout_counts(q, k, head_cfgs, block_size, stream, groups)
+    toff, coff = ctx["toff"], ctx["coff"]
+    totals = torch.stack([toff[-1], coff[-1]]).cpu()  # the host read-back that sizes the layout
     nt, nc = int(totals[0]), int(totals[1])
     tiles = torch.empty(max(nt, 1), dtype=torch.int32, device=dev)
     cols = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
-    for cfg, ids, m in groups:
-        if isinstance(cfg, VerticalSlash):
-            vert, sl = vs_sel[cfg]
-            layouts.vs_fill(vert, sl, ids, s_len, block_size, toff, coff, tiles, cols, stream)
-        elif isinstance(cfg, AShape):
-            layouts.ashape_fill(ids, m, s_len, block_size, cfg, toff, tiles, stream)
-        else:
-            estimate_block_sparse_gpu(q, k, cfg, ids, toff, tiles, stream)
-    return LayerLayout(s_len, block_size, hq, tiles[:nt], toff, cols[:nc], coff)
+    _layout_fill(q, k, ctx, block_size, tiles, cols, stream)
+    return LayerLayout(ctx["s_len"], block_size, ctx["hq"], tiles[:nt], toff, cols[:nc], coff)
+
+
+def build_layer_layout_into(q, k, head_cfgs, block_size, tiles_buf, cols_buf, overflow, totals, stream=None,
+                            groups=None):
+    """Estimation + compaction into caller-owned buffers of fixed capacity, with no host
+    sync: ``spf_csr_guard`` compares the totals with the capacities on the device and, if
+    they do not fit, empties every row (nothing is written past a buffer; the attention
+    then yields zero rows) and sets ``overflow`` (an int32 device scalar), while
+    ``totals`` (int64 [2] on the device) receives the true sizes.  The caller checks the
+    flag later and redoes an overflowed layer with ``build_layer_layout``."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return build_layer_layout_into(q, k, head_cfgs, block_size, tiles_buf, cols_buf, overflow, totals, None,
+                                           groups)
+    ctx = _layout_counts(q, k, head_cfgs, block_size, None, groups)
+    layouts.csr_guard(ctx["toff"], ctx["coff"], tiles_buf.numel(), cols_buf.numel(), overflow, totals)
+    _layout_fill(q, k, ctx, block_size, tiles_buf, cols_buf, None)
+    return LayerLayout(ctx["s_len"], block_size, ctx["hq"], tiles_buf, ctx["toff"], cols_buf, ctx["coff"])
 
 
 _PAIR_CACHE: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()

@@ -163,3 +163,51 @@ def test_pipelined_prefill_equals_serial_layers(P):
         torch.cuda.synchronize()
         assert torch.equal(outs[-1], want[-1])
     assert len(events) == 12 and all(a.elapsed_time(b) > 0 for a, b in events)
+
+
+@pytest.mark.gpu
+def test_speculative_csr_sizing_and_overflow_recovery(P):
+    """SparsePrefill.prefill (default): after the first call (exact sizes) layers are built
+    into speculatively sized buffers with no per-layer host sync; a layer whose layout no
+    longer fits is emptied on the device (spf_csr_guard), flagged and recomputed exactly --
+    the outputs always equal the per-layer results."""
+    import torch
+
+    from paper_2407_02490_b200 import _lib
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(21)
+    hq, hkv, s, d = 8, 2, 4096, 128
+    table = PatternTable([[P.VerticalSlash(64, 256)] * 5 + [P.AShape(64, 512), P.BlockSparse(8), P.VerticalSlash(16, 64)],
+                          [P.BlockSparse(6)] * 8,
+                          [P.VerticalSlash(200, 700)] * 8])
+    layers = [tuple(torch.randn(h, s, d, generator=g, device=dev).to(torch.bfloat16) for h in (hq, hkv, hkv))
+              for _ in range(3)]
+    model = SparsePrefill(table)
+    want = [model.layer(i, *layers[i]).clone() for i in range(3)]
+    for it in range(3):  # first call sizes exactly, then speculative
+        got = model.prefill(layers)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert torch.equal(got[i], want[i]), (it, i)
+    # force an overflow in every layer: capacities far below the true sizes
+    model._caps = {key: (7, 3) for key in model._caps}
+    seen = []
+    got = model.prefill(layers, after_layer=lambda layer, o: seen.append(layer))
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert torch.equal(got[i], want[i]), ("overflow", i)
+    assert seen == [0, 1, 2, 0, 1, 2]  # speculative outputs, then the recomputed ones
+    assert all(cap[0] > 7 for cap in model._caps.values())  # grown from the device totals
+    # and the guard itself: an emptied layout has all-zero offsets
+    toff = torch.tensor([0, 5, 9], dtype=torch.int64, device=dev)
+    coff = torch.tensor([0, 1, 2], dtype=torch.int64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    tot = torch.zeros(2, dtype=torch.int64, device=dev)
+    from paper_2407_02490_b200 import layouts
+
+    layouts.csr_guard(toff, coff, 8, 10, flag, tot)
+    torch.cuda.synchronize()
+    assert int(flag) == 1 and tot.tolist() == [9, 2] and toff.tolist() == [0, 0, 0] and coff.tolist() == [0, 0, 0]
+    assert "spf_csr_guard" not in _lib.missing_symbols()

@@ -358,10 +358,13 @@ constexpr int kFbThreads = 256;
 
 template <int kD>
 struct FbSmem {
-  static constexpr int kLd = kD + 4;                // doubles per staged row (2-wavefront fragment loads)
-  static constexpr int kOffQ = 0;                   // double [64][kLd]
-  static constexpr int kOffK = kOffQ + 64 * kLd * 8;
-  static constexpr int kOffP = kOffK + 64 * kLd * 8;  // float [64][65] (pass B)
+  // Q and K rows staged as bf16 (converted to fp64 at fragment load): 17 KB each, so two
+  // CTAs fit per SM.  The 8-element pad puts the 8 rows a fragment load touches on
+  // distinct banks.
+  static constexpr int kLd = kD + 8;                // bf16 per staged row
+  static constexpr int kOffQ = 0;                   // bf16 [64][kLd]
+  static constexpr int kOffK = kOffQ + 64 * kLd * 2;
+  static constexpr int kOffP = kOffK + 64 * kLd * 2;  // float [64][65] (pass B)
   static constexpr int kOffCol = kOffP + 64 * 65 * 4;  // double [64]
   static constexpr int kOffDiag = kOffCol + 64 * 8;    // double [127]
   static constexpr int kOffRed = kOffDiag + 128 * 8;   // double [2][64] (cross-warp row reductions)
@@ -388,36 +391,36 @@ __device__ __forceinline__ void fb_fetch(const __nv_bfloat16* src, int valid, in
   }
 }
 template <int kD>
-__device__ __forceinline__ void fb_store(double* dst, const int4 (&r)[kD / 32]) {
+__device__ __forceinline__ void fb_store(__nv_bfloat16* dst, const int4 (&r)[kD / 32]) {
 #pragma unroll
   for (int u = 0; u < kD / 32; ++u) {
     const int ch = threadIdx.x + u * kFbThreads;
     const int row = ch / (kD / 8), c8 = ch % (kD / 8);
-    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&r[u]);
-    double2* o = reinterpret_cast<double2*>(dst + row * FbSmem<kD>::kLd + c8 * 8);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) o[e] = make_double2(__bfloat162float(x[2 * e]), __bfloat162float(x[2 * e + 1]));
+    *reinterpret_cast<int4*>(dst + row * FbSmem<kD>::kLd + c8 * 8) = r[u];
   }
 }
 
+__device__ __forceinline__ double bf16_to_f64(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
+
 // acc[mi][ni] = 8x8 tiles of Q K^T: rows m0 + 8 mi (+ lane / 4), keys n0 + 8 ni (+ 2 (lane % 4) + {0, 1})
 template <int kD>
-__device__ __forceinline__ void fb_scores(const double* Qs, const double* Ks, int m0, int n0, double (&acc)[2][4][2]) {
+__device__ __forceinline__ void fb_scores(const __nv_bfloat16* Qs, const __nv_bfloat16* Ks, int m0, int n0,
+                                          double (&acc)[2][4][2]) {
   constexpr int kLd = FbSmem<kD>::kLd;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  const double* qa = Qs + (m0 + (lane >> 2)) * kLd + (lane & 3);
-  const double* kb = Ks + (n0 + (lane >> 2)) * kLd + (lane & 3);
+  const __nv_bfloat16* qa = Qs + (m0 + (lane >> 2)) * kLd + (lane & 3);
+  const __nv_bfloat16* kb = Ks + (n0 + (lane >> 2)) * kLd + (lane & 3);
 #pragma unroll 8
   for (int ks = 0; ks < kD / 4; ++ks) {
     double a[2], b[4];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) a[mi] = qa[mi * 8 * kLd + 4 * ks];
+    for (int mi = 0; mi < 2; ++mi) a[mi] = bf16_to_f64(qa[mi * 8 * kLd + 4 * ks]);
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = kb[ni * 8 * kLd + 4 * ks];
+    for (int ni = 0; ni < 4; ++ni) b[ni] = bf16_to_f64(kb[ni * 8 * kLd + 4 * ks]);
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -426,12 +429,12 @@ __device__ __forceinline__ void fb_scores(const double* Qs, const double* Ks, in
 }
 
 template <int kD, int kPass>
-__global__ void __launch_bounds__(kFbThreads, 1) vs_fb_kernel(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(kFbThreads, 2) vs_fb_kernel(const __nv_bfloat16* __restrict__ q,
                                                               const __nv_bfloat16* __restrict__ k, const ExArgs a) {
   using SM = FbSmem<kD>;
   extern __shared__ __align__(16) uint8_t smraw[];
-  double* Qs = reinterpret_cast<double*>(smraw + SM::kOffQ);
-  double* Ks = reinterpret_cast<double*>(smraw + SM::kOffK);
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smraw + SM::kOffQ);
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw + SM::kOffK);
   float(*Ps)[65] = reinterpret_cast<float(*)[65]>(smraw + SM::kOffP);
   double* colsum = reinterpret_cast<double*>(smraw + SM::kOffCol);
   double* red = reinterpret_cast<double*>(smraw + SM::kOffRed);
@@ -725,9 +728,9 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
     note_launches(6);  // prep, list, pass A, combine, pass B, top-k
     vs_exact_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
     vs_exact_list_kernel<<<(unsigned)n_heads, kListThreads, 0, st>>>(a);
-    k1<<<148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
+    k1<<<2 * 148, kFbThreads, fb_smem, st>>>(qb, kbp, a);  // two CTAs per SM
     vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
-    k2<<<148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
+    k2<<<2 * 148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
     vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
                                                                                       k_s, gate, vout, sout);
     return check_cuda(cudaGetLastError(), "vs fallback");

@@ -191,6 +191,79 @@ __global__ void __launch_bounds__(kScore2Threads, 4) bs_score_tri_kernel(
   }
 }
 
+// The same scores on the fp64 tensor cores (DMMA mma.sync m8n8k4 f64; 37 TF/s vs ~20 for the
+// FMA kernel above, benchmarks/mb_dmma.cu) for d = 64 / 128: the block-causal tile's 64 pooled
+// rows of Q and K staged as fp32 (exact: the pooled means are fp32) with a 4-float pad (the
+// 8 rows a fragment load touches fall on distinct banks), converted to fp64 at fragment load;
+// 4 warps, each 16 rows x 64 columns (16 accumulators); three CTAs per SM.
+constexpr int kScoreDmmaThreads = 128;
+
+template <int kD>
+__global__ void __launch_bounds__(kScoreDmmaThreads, 3) bs_score_dmma_kernel(
+    const float* __restrict__ qp, const float* __restrict__ kp, const int32_t* __restrict__ head_ids,
+    int heads_per_kv, int N, double scale, double* __restrict__ out) {
+  constexpr int kLd = kD + 4;
+  extern __shared__ __align__(16) float sm_f[];
+  float* As = sm_f;
+  float* Bs = sm_f + kTile * kLd;
+  const int hi = blockIdx.y;
+  const int h = head_ids ? head_ids[hi] : hi;
+  const int kvh = h / heads_per_kv;
+  const int t = blockIdx.x;  // lower-triangle tile t -> (at, bt), bt <= at
+  int at = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((at + 1) * (at + 2) / 2 <= t) ++at;
+  while (at * (at + 1) / 2 > t) --at;
+  const int bt = t - at * (at + 1) / 2;
+  const int a0 = at * kTile, b0 = bt * kTile;
+  const float* Ah = qp + ((int64_t)h * N + a0) * kD;
+  const float* Bh = kp + ((int64_t)kvh * N + b0) * kD;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < kTile * (kD / 4); e += kScoreDmmaThreads) {
+    const int r = e / (kD / 4), c4 = (e % (kD / 4)) * 4;
+    const float4 a = a0 + r < N ? *reinterpret_cast<const float4*>(Ah + (int64_t)r * kD + c4) : make_float4(0, 0, 0, 0);
+    const float4 b = b0 + r < N ? *reinterpret_cast<const float4*>(Bh + (int64_t)r * kD + c4) : make_float4(0, 0, 0, 0);
+    *reinterpret_cast<float4*>(As + r * kLd + c4) = a;
+    *reinterpret_cast<float4*>(Bs + r * kLd + c4) = b;
+  }
+  __syncthreads();
+  double acc[2][8][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const float* qa = As + (16 * warp + (lane >> 2)) * kLd + (lane & 3);
+  const float* kb = Bs + (lane >> 2) * kLd + (lane & 3);
+#pragma unroll 4
+  for (int ks = 0; ks < kD / 4; ++ks) {
+    double a[2], b[8];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) a[mi] = (double)qa[mi * 8 * kLd + 4 * ks];
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni) b[ni] = (double)kb[ni * 8 * kLd + 4 * ks];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 8; ++ni)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+                     : "d"(a[mi]), "d"(b[ni]));
+  }
+  double* outh = out + (int64_t)hi * N * N;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+    const int a = a0 + 16 * warp + 8 * mi + (lane >> 2);
+    if (a >= N) continue;
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni) {
+      const int b = b0 + 8 * ni + 2 * (lane & 3);
+      const double v0 = (b <= a) ? scale * acc[mi][ni][0] : -INFINITY;
+      const double v1 = (b + 1 <= a) ? scale * acc[mi][ni][1] : -INFINITY;
+      if (b + 1 < N) *reinterpret_cast<double2*>(outh + (int64_t)a * N + b) = make_double2(v0, v1);
+      else if (b < N) outh[(int64_t)a * N + b] = v0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- Block-Sparse
 template <typename T>
 __global__ void pool_kernel(const T* __restrict__ x, int64_t n_rows_total, int S, int d, int B,
@@ -322,7 +395,26 @@ int bs_estimate_impl(const T* q, const T* k, int Hq, int Hkv, int S, int d, cons
   }
   const int nt = (N + kTile - 1) / kTile;
   note_launches(1);
-  if (d % 4 == 0)
+  if ((d == 128 || d == 64) && N % 2 == 0) {  // fp64 tensor cores (double2 stores need an even row length)
+    const unsigned grid_t = (unsigned)(nt * (nt + 1) / 2);
+    const int smem = 2 * kTile * (d + 4) * (int)sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      if ((rc = check_cuda(cudaFuncSetAttribute(bs_score_dmma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                2 * kTile * (128 + 4) * 4), "bs score smem")))
+        return rc;
+      if ((rc = check_cuda(cudaFuncSetAttribute(bs_score_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                2 * kTile * (64 + 4) * 4), "bs score smem")))
+        return rc;
+      attr = true;
+    }
+    if (d == 128)
+      bs_score_dmma_kernel<128><<<dim3(grid_t, (unsigned)n_heads), kScoreDmmaThreads, smem, st>>>(
+          qp, kp, head_ids, Hq / Hkv, N, 1.0 / sqrt((double)d), sc);
+    else
+      bs_score_dmma_kernel<64><<<dim3(grid_t, (unsigned)n_heads), kScoreDmmaThreads, smem, st>>>(
+          qp, kp, head_ids, Hq / Hkv, N, 1.0 / sqrt((double)d), sc);
+  } else if (d % 4 == 0)
     bs_score_tri_kernel<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)n_heads), kScore2Threads, 0, st>>>(
         qp, kp, head_ids, Hq / Hkv, N, d, 1.0 / sqrt((double)d), sc);
   else

@@ -322,6 +322,45 @@ class SparsePrefill:
                             after_layer(layer, results[layer])
         return results
 
+    def graph_layer(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor):
+        """Capture one layer (estimation, compaction into a fixed-capacity CSR, attention) in a
+        CUDA graph over the static buffers ``q``, ``k``, ``v``, ``out``; returns ``replay()``,
+        which re-runs the layer on whatever those buffers then hold and returns the overflow
+        flag (an int32 device scalar: 1 = the layout outgrew the captured capacity and ``out``
+        is not valid; re-capture after an exact run).  The layer is first run eagerly to size
+        the CSR (with the same +12.5 % slack as ``prefill``) and to finish one-time setup."""
+        dev = q.device
+        cfgs = self.table.layer(layer)
+        b = self.table.block_size(layer, self.default_block)
+        groups = self.table.device_groups(layer, dev)
+        lay = build_layer_layout(q, k, cfgs, b, groups=groups)
+        nt, nc = lay.n_tiles + lay.n_tiles // 8 + 64, lay.n_cols + lay.n_cols // 8 + 64
+        tiles = torch.empty(nt, dtype=torch.int32, device=dev)
+        cols = torch.empty(nc, dtype=torch.int32, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        totals = torch.zeros(2, dtype=torch.int64, device=dev)
+
+        def body():
+            lay2 = build_layer_layout_into(q, k, cfgs, b, tiles, cols, flag, totals, groups=groups)
+            self._attend(layer, q, k, v, lay2, b, out, torch.cuda.current_stream(dev), None)
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up on the capture stream (workspaces, attributes)
+            body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            flag.zero_()
+            body()
+
+        def replay():
+            graph.replay()
+            return flag
+
+        replay.graph = graph
+        return replay
+
     def _prefill_pipelined(self, layers, outs, attn_events, after_layer):
         dev = layers[0][0].device
         comp = torch.cuda.current_stream(dev)

@@ -335,26 +335,34 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     };
 
     // gather 64 rows (16-byte chunks) of K or V by column index into a SW128 tile
-    auto gather = [&](uint8_t* dst, const __nv_bfloat16* src, const __nv_bfloat16* src2, const StepInfo& st) {
+    // gather 64 rows (16-byte chunks) of K or V by column index into a SW128 tile: every
+    // lane's cp.async copies are in flight at once (rows past the chip are zero-filled) and
+    // complete into the stage's mbarrier (cp.async.mbarrier.arrive, then lane 0's arrival),
+    // so the loader goes on to the next step instead of waiting; the MMA warp fences the
+    // async proxy after the barrier (benchmarks/bench_columns.py: a chip step cost ~13x a
+    // tile step with per-chunk __ldg round trips)
+    auto gather = [&](uint8_t* dst, const __nv_bfloat16* src, const __nv_bfloat16* src2, const StepInfo& st,
+                      uint64_t* bar) {
       constexpr int kChunksPerRow = kD / 8;
+      // the chip's column indices: lane l holds keys l and l + 32
+      const int key_a = lane < st.n ? p.col_indices[st.s0 + lane] : 0;
+      const int key_b = lane + 32 < st.n ? p.col_indices[st.s0 + lane + 32] : 0;
+      const uint32_t dbase = smem_u32(dst);
+#pragma unroll 8
       for (int idx = lane; idx < kBox * kChunksPerRow; idx += 32) {
         const int j = idx / kChunksPerRow;
         const int c16 = idx % kChunksPerRow;
         const int atom = c16 >> 3, c = c16 & 7;
         const uint32_t off = atom * (kBox * 128) + (j >> 3) * 1024 + (j & 7) * 128 + ((c ^ (j & 7)) << 4);
-        int4 x = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
-        if (j < st.n) {
-          const int key = p.col_indices[st.s0 + j];
-          const int64_t e = (int64_t)key * kD + c16 * 8;
-          x = __ldg(reinterpret_cast<const int4*>(src + e));
-          if (kSplit) x2 = __ldg(reinterpret_cast<const int4*>(src2 + e));
-        }
-        *reinterpret_cast<int4*>(dst + off) = x;
-        if (kSplit) *reinterpret_cast<int4*>(dst + L::kKBytes + off) = x2;
+        const int kj = __shfl_sync(0xffffffffu, j < 32 ? key_a : key_b, j & 31);
+        const bool valid = j < st.n;
+        const int64_t e = (int64_t)(valid ? kj : 0) * kD + c16 * 8;
+        cp_async_16_zfill(dbase + off, src + e, valid);
+        if (kSplit) cp_async_16_zfill(dbase + L::kKBytes + off, src2 + e, valid);
       }
-      fence_proxy_async_smem();
-      __threadfence_block();
+      cp_async_mbar_arrive(bar);  // this lane's copies arrive on the barrier when they land
       __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
     };
 
     int running = INT_MIN;  // chip prefix max, carried across a chip's 64-key steps
@@ -408,8 +416,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
           }
         }
       } else {
-        gather(kst, kb, kb2, st);
-        if (lane == 0) mbar_arrive(&ctrl->k_full[sk]);
+        gather(kst, kb, kb2, st, &ctrl->k_full[sk]);
       }
       __syncwarp();
       write_desc(t, st);
@@ -421,8 +428,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
       if (lane == 0) mbar_wait(&ctrl->v_empty[sv], ((t / R::kV) & 1) ^ 1);
       __syncwarp();
       if (st.kind == kChip) {
-        gather(vst, vb, vb2, st);
-        if (lane == 0) mbar_arrive(&ctrl->v_full[sv]);
+        gather(vst, vb, vb2, st, &ctrl->v_full[sv]);
       } else if (lane == 0) {
         mbar_arrive_expect_tx(&ctrl->v_full[sv], L::kTxKV);
 #pragma unroll
@@ -471,6 +477,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         const int sv = u % R::kV;
         mbar_wait(&ctrl->p_full[u & 1], (u >> 1) & 1);
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
+        fence_proxy_async_smem();  // gathered (cp.async) chips: generic-proxy writes -> tcgen05 reads
         tc_fence_after();
         const uint32_t vd = vlo0 + ((sv * kStageKV) >> 4);
         // P(u): own columns (separate-P) or over S(u) (split: hi in cols 0..31, lo in 32..63)
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         const int sk = t % R::kK;
         const int sb = kSepP<kSplit> ? 0 : t & 1;
         mbar_wait(&ctrl->k_full[sk], (t / R::kK) & 1);
+        fence_proxy_async_smem();
         if (kSepP<kSplit>) {
           if (t > 0) mbar_wait(&ctrl->s_free[0], (t - 1) & 1);  // softmax(t-1) has read S
         } else {

@@ -276,14 +276,19 @@ class SparsePrefill:
         totals = torch.zeros((n_layers, 2), dtype=torch.int64, device=dev)
         keys = [(layer, tuple(q.shape), tuple(k.shape), str(dev)) for layer, (q, k, _) in enumerate(layers)]
 
+        if not hasattr(self, "_arenas"):
+            self._arenas = {}
+        akey = (str(dev), int(comp.cuda_stream))  # one buffer pair per stream: passes on two streams never share
+
         def arena(nt, nc):
-            cur = getattr(self, "_arena", None)
-            if cur is None or cur[0].device != dev or cur[0].numel() < nt or cur[1].numel() < nc:
-                nt2 = max(nt, cur[0].numel() if cur is not None and cur[0].device == dev else 0)
-                nc2 = max(nc, cur[1].numel() if cur is not None and cur[1].device == dev else 0)
-                self._arena = (torch.empty(max(nt2, 1), dtype=torch.int32, device=dev),
-                               torch.empty(max(nc2, 1), dtype=torch.int32, device=dev))
-            return self._arena
+            cur = self._arenas.get(akey)
+            if cur is None or cur[0].numel() < nt or cur[1].numel() < nc:
+                nt2 = max(nt, cur[0].numel() if cur is not None else 0)
+                nc2 = max(nc, cur[1].numel() if cur is not None else 0)
+                cur = (torch.empty(max(nt2, 1), dtype=torch.int32, device=dev),
+                       torch.empty(max(nc2, 1), dtype=torch.int32, device=dev))
+                self._arenas[akey] = cur
+            return cur
 
         speculated = []
         results = []

@@ -44,6 +44,21 @@ def main():
     lay32 = P.build_layer_layout(qf, kf, [P.VerticalSlash(32, 128)] * hq, 64)
     kernels.sparse_flash_attention_gpu(qf, kf, vf, 1 / math.sqrt(d), 64, lay32.tiles, lay32.tile_offsets,
                                        lay32.cols, lay32.col_offsets)
+    # round-2 paths: G-local heads (rigorous bound -> the DMMA fp64 fallback), a column-heavy
+    # layout (cp.async chip gathers), the speculative model pass with an overflow (CSR guard),
+    # Block-Sparse pooled scores on DMMA (even block count)
+    from benchmarks.workloads import g_local_qkv
+    from paper_2407_02490_b200.driver import PatternTable, SparsePrefill
+
+    ql, kl, vl = g_local_qkv(hq, hkv, s, d, seed=1, device=dev)
+    vs_estimate_async(ql, kl, P.VerticalSlash(100, 300), mode="fast")
+    lay_c = P.build_layer_layout(q, k, [P.VerticalSlash(600, 16)] * hq, 64)
+    kernels.sparse_flash_attention_gpu(q, k, v, 1 / math.sqrt(d), 64, lay_c.tiles, lay_c.tile_offsets, lay_c.cols,
+                                       lay_c.col_offsets)
+    model = SparsePrefill(PatternTable([cfgs, [P.BlockSparse(6)] * hq]))
+    model.prefill([(q, k, v), (ql, kl, vl)])
+    model._caps = {key: (5, 3) for key in model._caps}
+    model.prefill([(q, k, v), (ql, kl, vl)])
     torch.cuda.synchronize()
     assert bool(torch.isfinite(out).all()) and bool(torch.isfinite(lse).all())
     print("sanitize smoke ok")

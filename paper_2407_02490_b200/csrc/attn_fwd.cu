@@ -336,11 +336,10 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
 
     // gather 64 rows (16-byte chunks) of K or V by column index into a SW128 tile
     // gather 64 rows (16-byte chunks) of K or V by column index into a SW128 tile: every
-    // lane's cp.async copies are in flight at once (rows past the chip are zero-filled) and
-    // complete into the stage's mbarrier (cp.async.mbarrier.arrive, then lane 0's arrival),
-    // so the loader goes on to the next step instead of waiting; the MMA warp fences the
-    // async proxy after the barrier (benchmarks/bench_columns.py: a chip step cost ~13x a
-    // tile step with per-chunk __ldg round trips)
+    // lane's cp.async copies are in flight at once (rows past the chip are zero-filled), one
+    // wait, a proxy fence, then lane 0's arrival (benchmarks/bench_columns.py: a chip step
+    // cost ~13x a tile step with per-chunk __ldg round trips; completing the copies into the
+    // mbarrier asynchronously gained only 3 % more and draws synccheck "missing wait" reports)
     auto gather = [&](uint8_t* dst, const __nv_bfloat16* src, const __nv_bfloat16* src2, const StepInfo& st,
                       uint64_t* bar) {
       constexpr int kChunksPerRow = kD / 8;
@@ -360,7 +359,9 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         cp_async_16_zfill(dbase + off, src + e, valid);
         if (kSplit) cp_async_16_zfill(dbase + L::kKBytes + off, src2 + e, valid);
       }
-      cp_async_mbar_arrive(bar);  // this lane's copies arrive on the barrier when they land
+      cp_async_wait_all();
+      fence_proxy_async_smem();
+      __threadfence_block();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar);
     };
@@ -477,7 +478,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         const int sv = u % R::kV;
         mbar_wait(&ctrl->p_full[u & 1], (u >> 1) & 1);
         mbar_wait(&ctrl->v_full[sv], (u / R::kV) & 1);
-        fence_proxy_async_smem();  // gathered (cp.async) chips: generic-proxy writes -> tcgen05 reads
         tc_fence_after();
         const uint32_t vd = vlo0 + ((sv * kStageKV) >> 4);
         // P(u): own columns (separate-P) or over S(u) (split: hi in cols 0..31, lo in 32..63)
@@ -505,7 +505,6 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
         const int sk = t % R::kK;
         const int sb = kSepP<kSplit> ? 0 : t & 1;
         mbar_wait(&ctrl->k_full[sk], (t / R::kK) & 1);
-        fence_proxy_async_smem();
         if (kSepP<kSplit>) {
           if (t > 0) mbar_wait(&ctrl->s_free[0], (t - 1) & 1);  // softmax(t-1) has read S
         } else {

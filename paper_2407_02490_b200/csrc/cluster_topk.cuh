@@ -63,15 +63,41 @@ struct ClusterTopK {
 
   // vals: n values in global memory (the whole vector); writes min(k, n) indices.
   // tau != nullptr: certification; sets *flag |= 1 when the selection is too close to call.
+  // [lo, hi) (optional, hi > lo): every value outside is known to be +0 (the fp64 fallback's
+  // support); the selection then scans only [lo, hi) when at least k values there are
+  // positive -- the k-th largest is then positive, so nothing outside is selected -- and the
+  // whole vector otherwise (zeros are then taken by lowest index over all of it).
   static __device__ void run(Storage& sm, const double* __restrict__ vals, int n, int k, bool descending,
-                             int32_t* out, const float* tau, int32_t* flag) {
+                             int32_t* out, const float* tau, int32_t* flag, int lo = 0, int hi = -1) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     const int tid = threadIdx.x;
     if (k > n) k = n;
-    const int chunk = (n + kCl - 1) / kCl;
-    const int s0 = min(n, rank * chunk), s1 = min(n, s0 + chunk);
+    int dlo = 0, dhi = n;
+    if (hi > lo && (lo > 0 || hi < n) && hi - lo >= k) {
+      const int c = (hi - lo + kCl - 1) / kCl;
+      const int a0 = min(hi, lo + rank * c), a1 = min(hi, a0 + c);
+      int pos = 0;
+      for (int i = a0 + tid; i < a1; i += kThreads) pos += vals[i] > 0.0 ? 1 : 0;
+      int excl, pos_cta;
+      Scan(sm.scan).ExclusiveSum(pos, excl, pos_cta);
+      if (tid == 0) *cl.map_shared_rank(&sm.cnt[0][rank], 0) = pos_cta;
+      cl.sync();
+      if (rank == 0 && tid == 0) {
+        int total = 0;
+        for (int r = 0; r < kCl; ++r) total += sm.cnt[0][r];
+        for (int r = 0; r < kCl; ++r) *cl.map_shared_rank(&sm.ncand, r) = total >= k ? 1 : 0;
+      }
+      cl.sync();
+      if (sm.ncand) {  // cluster-uniform
+        dlo = lo;
+        dhi = hi;
+      }
+      __syncthreads();
+    }
+    const int chunk = (dhi - dlo + kCl - 1) / kCl;
+    const int s0 = min(dhi, dlo + rank * chunk), s1 = min(dhi, s0 + chunk);
     if (rank == 0)
       for (int b = tid; b < 2 * kBins; b += kThreads) (&sm.tot[0][0])[b] = 0;
     cl.sync();

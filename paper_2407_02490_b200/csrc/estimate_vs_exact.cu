@@ -627,15 +627,26 @@ constexpr int kTopkCl = 8;
 __global__ void __cluster_dims__(kTopkCl, 1, 1) __launch_bounds__(kTopkThreads)
     vs_exact_topk_kernel(const double* __restrict__ vscore, const double* __restrict__ sscore, int S, int k_v,
                          int k_s, const int32_t* gate, int32_t* __restrict__ vert_out,
-                         int32_t* __restrict__ slash_out) {
+                         int32_t* __restrict__ slash_out, const int32_t* __restrict__ list,
+                         const int32_t* __restrict__ head_count, int n_kblk, int KB, int L) {
   using TK = ClusterTopK<kTopkThreads, kTopkCl>;
   __shared__ typename TK::Storage sm;
   const int hi = blockIdx.y;
   if (gate != nullptr && gate[hi] == 0) return;  // cluster-uniform
+  // fallback heads: only the listed items carry nonzero vertical scores, and only the
+  // diagonals through them nonzero slash scores (everything else was written +0 by prep)
+  int lo_v = 0, hi_v = -1, lo_s = 0, hi_s = -1;
+  if (list != nullptr && head_count[hi] > 0) {
+    const int32_t* lh = list + (int64_t)hi * n_kblk;  // ascending (vs_exact_list_kernel)
+    lo_v = lh[0] * KB;
+    hi_v = min(S, (lh[head_count[hi] - 1] + 1) * KB);
+    lo_s = max(0, S - L - (hi_v - 1));  // offset o = (S - L + i) - j, i in [0, L), j in [lo_v, hi_v)
+    hi_s = min(S, S - lo_v);
+  }
   if (blockIdx.z == 0)
-    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, false, vert_out + (int64_t)hi * k_v, nullptr, nullptr);
+    TK::run(sm, vscore + (int64_t)hi * S, S, k_v, false, vert_out + (int64_t)hi * k_v, nullptr, nullptr, lo_v, hi_v);
   else
-    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, true, slash_out + (int64_t)hi * k_s, nullptr, nullptr);
+    TK::run(sm, sscore + (int64_t)hi * S, S, k_s, true, slash_out + (int64_t)hi * k_s, nullptr, nullptr, lo_s, hi_s);
 }
 
 int kb_for(int L) { return kKeyT * max(1, (L - 1 + kKeyT - 1) / kKeyT); }
@@ -731,8 +742,8 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
     k1<<<2 * 148, kFbThreads, fb_smem, st>>>(qb, kbp, a);  // two CTAs per SM
     vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
     k2<<<2 * 148, kFbThreads, fb_smem, st>>>(qb, kbp, a);
-    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
-                                                                                      k_s, gate, vout, sout);
+    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(
+        a.vscore, a.sscore, S, k_v, k_s, gate, vout, sout, a.list, a.head_count, a.n_kblk, a.KB, L);
     return check_cuda(cudaGetLastError(), "vs fallback");
   }
   a.tile_max = nullptr;  // the full fp64 path visits every item
@@ -747,8 +758,8 @@ int vs_exact_run(int dtype, const void* q, const void* k, int Hq, int Hkv, int S
     k1<<<grid, kThreads, smem, st>>>(qq, kk, a);
     vs_exact_combine_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)n_heads), 256, 0, st>>>(a);
     k2<<<grid, kThreads, smem, st>>>(qq, kk, a);
-    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(a.vscore, a.sscore, S, k_v,
-                                                                                      k_s, gate, vout, sout);
+    vs_exact_topk_kernel<<<dim3(kTopkCl, (unsigned)n_heads, 2), kTopkThreads, 0, st>>>(
+        a.vscore, a.sscore, S, k_v, k_s, gate, vout, sout, nullptr, nullptr, 0, 0, L);
     return check_cuda(cudaGetLastError(), "vs exact");
   };
   if (dtype == SPF_DTYPE_BF16)

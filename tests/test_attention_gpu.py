@@ -190,6 +190,54 @@ def test_paired_box_kernel_matches_oracle(K, s, kb, d, routing):
         assert np.abs(got[h] - union[h]).max() < BF16_TOL
 
 
+@pytest.mark.parametrize("s,kb,jump", [(1000, 5, 0.0), (4097, 8, 40.0), (2049, 64, 160.0), (200, 3, 160.0)])
+def test_block_sparse_kernel_sink_and_lse(K, s, kb, jump):
+    """Block-Sparse heads routed by pair_heads (paired-box kernel; also the parity test the
+    transposed-step experiment, benchmarks/experiments/attn_bst.cu, passed) on layouts whose
+    every row also takes block 0, with key 0 made a sink `jump` above the rest (20 and 81 in
+    log2 units: the running maxima must be raised after the diagonal step, O and the row sums
+    rescaled).  Rows with an odd tile count, a partial last block and kb beyond the row
+    length.  Output and the per-row log-sum-exp equal the oracle's."""
+    hq, hkv, b, d = 4, 2, 64, 128
+    rng = np.random.Generator(np.random.PCG64(s + kb))
+    q = rng.standard_normal((hq, s, d)).astype(np.float32)
+    k = rng.standard_normal((hkv, s, d)).astype(np.float32)
+    v = rng.standard_normal((hkv, s, d)).astype(np.float32)
+    q[..., 0] = 4.0
+    k[:, 0, 0] = jump
+    q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
+    n = (s + b - 1) // b
+    tiles_all = []
+    for h in range(hq):
+        for r in range(n):
+            m = min(kb, r + 1)
+            blocks = set(rng.choice(r + 1, size=m, replace=False).tolist()) | {0, r}
+            tiles_all.append(sorted(x * b for x in blocks))
+    ts, to = port.flatten(tiles_all)
+    co = np.zeros(hq * n + 1, np.int64)
+    dev = torch.device("cuda")
+    args = (torch.from_numpy(q).to(dev, torch.bfloat16), torch.from_numpy(k).to(dev, torch.bfloat16),
+            torch.from_numpy(v).to(dev, torch.bfloat16), 1 / math.sqrt(d), b,
+            torch.from_numpy(ts.astype(np.int32)).to(dev), torch.from_numpy(to).to(dev),
+            torch.zeros(1, dtype=torch.int32, device=dev), torch.from_numpy(co).to(dev))
+    lse = torch.empty(hq, s, dtype=torch.float32, device=dev)
+    got = K.sparse_flash_attention_gpu(*args, lse=lse, pair_heads=torch.arange(hq, dtype=torch.int32, device=dev))
+    got = got.float().cpu().numpy()
+    lse = lse.cpu().numpy()
+    for h in range(hq):
+        kvh = h // (hq // hkv)
+        tt, tto = port.flatten(tiles_all[h * n:(h + 1) * n])
+        want = port.sparse_flash_rows(q[h], k[kvh], v[kvh], 1 / math.sqrt(d), b, tt, tto,
+                                      np.zeros(0, np.int64), np.zeros(n + 1, np.int64))
+        assert np.abs(got[h] - want).max() < BF16_TOL, (h, np.abs(got[h] - want).max())
+        mask = port.layout_to_mask(s, b, tiles_all[h * n:(h + 1) * n], [[] for _ in range(n)])
+        sc = (q[h].astype(np.float64) @ k[kvh].astype(np.float64).T) / math.sqrt(d)
+        sc = np.where(mask, sc, -np.inf)
+        mx = sc.max(axis=1)
+        want_lse = mx + np.log(np.exp(sc - mx[:, None]).sum(axis=1))
+        assert np.abs(lse[h] - want_lse).max() < 1e-2 * max(1.0, np.abs(want_lse).max()), h
+
+
 def test_pair_heads_validation(K):
     dev = torch.device("cuda")
     q = torch.zeros(2, 128, 64, dtype=torch.bfloat16, device=dev)

@@ -34,6 +34,24 @@ __device__ __forceinline__ int head_of(const int32_t* head_ids, int i) { return 
 // start, else absorbed) 32 at a time with ballots.
 constexpr int kMergeWarps = 8;
 
+// Warp-wide partition point: the number of leading indices of [lo, hi) for which `pred` holds
+// (pred true on a prefix), in ceil(log32(hi - lo)) rounds of 32 probes instead of a binary
+// search's dependent loads.
+template <class Pred>
+__device__ __forceinline__ int warp_partition_point(int lo, int hi, int lane, Pred pred) {
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int p = lo + lane * step;
+    const int c = __popc(__ballot_sync(0xffffffffu, p < hi && pred(p)));
+    if (c == 0) return lo;
+    const int nhi = min(hi, lo + c * step);  // probe c (if inside) failed
+    lo += (c - 1) * step + 1;                // probe c - 1 held
+    hi = nhi;
+  }
+  const int p = lo + lane;
+  return lo + __popc(__ballot_sync(0xffffffffu, p < hi && pred(p)));
+}
+
 template <bool kFill>
 __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
     const int32_t* __restrict__ vertical, int n_v, const int32_t* __restrict__ slash, int n_s,
@@ -49,31 +67,46 @@ __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
   const int32_t* sl = slash + (int64_t)i * n_s;
   const bool staged = n_v + 2 * n_s <= kSmemIdx;
   int32_t* gaps = s_idx + n_v + n_s;
+  __shared__ int s_wgap[kMergeWarps];
   if (staged) {
+#pragma unroll 4
     for (int j = threadIdx.x; j < n_v; j += blockDim.x) s_idx[j] = pts[j];
+#pragma unroll 4
     for (int j = threadIdx.x; j < n_s; j += blockDim.x) s_idx[n_v + j] = sl[j];
     __syncthreads();
     pts = s_idx;
     sl = s_idx + n_v;
     // gap list: slash indices j whose range starts past the previous range's end in every
-    // full row (o[j-1] - o[j] > B); only these can end a coalesced group
-    if (threadIdx.x < 32) {
-      const int ln = threadIdx.x;
-      int n = 0;
-      for (int b0 = 1; b0 < n_s; b0 += 32) {
-        const int j = b0 + ln;
-        const bool g = j < n_s && sl[j - 1] - sl[j] > B;
-        const unsigned m = __ballot_sync(0xffffffffu, g);
-        if (g) gaps[n + __popc(m & ((1u << ln) - 1u))] = j;
-        n += __popc(m);
-      }
-      if (ln == 0) s_ngap = n;
+    // full row (o[j-1] - o[j] > B); only these can end a coalesced group.  Each warp lists a
+    // contiguous chunk of [1, n_s) (count, block prefix, write), in ascending order.
+    const int wg = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const int chunk = (((n_s - 1 + kMergeWarps - 1) / kMergeWarps) + 31) & ~31;
+    const int j0 = 1 + wg * chunk, j1 = min(n_s, j0 + chunk);
+    int n = 0;
+    for (int b0 = j0; b0 < j1; b0 += 32) {
+      const int j = b0 + ln;
+      n += __popc(__ballot_sync(0xffffffffu, j < j1 && sl[j - 1] - sl[j] > B));
     }
+    if (ln == 0) s_wgap[wg] = n;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wg; ++w) base += s_wgap[w];
+    for (int b0 = j0; b0 < j1; b0 += 32) {
+      const int j = b0 + ln;
+      const bool g = j < j1 && sl[j - 1] - sl[j] > B;
+      const unsigned m = __ballot_sync(0xffffffffu, g);
+      if (g) gaps[base + __popc(m & ((1u << ln) - 1u))] = j;
+      base += __popc(m);
+    }
+    if (wg == kMergeWarps - 1 && ln == 0) s_ngap = base;
     __syncthreads();
   }
   const int n_gap = staged ? s_ngap : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
+  // ceil(x / B) for x > -B without an integer division when B is a power of two (B = 64)
+  const int bsh = (B & (B - 1)) == 0 ? __ffs(B) - 1 : -1;
+  auto ceil_div = [=](int x) { return bsh >= 0 && x >= 0 ? (x + B - 1) >> bsh : (x + B - 1) / B; };
   const int r_end = min(n_rows, (blockIdx.x + 1) * rows_per_cta);
   for (int r = blockIdx.x * rows_per_cta + warp; r < r_end; r += kMergeWarps) {
     const int64_t row = (int64_t)h * n_rows + r;
@@ -86,42 +119,38 @@ __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
     int jv = 0;
     // flush a group [fs, fe): points < its cover end are consumed (columns if < fs), then its tiles
     auto flush = [&](int fs, int fe, bool with_tiles) {
-      const int cover = with_tiles ? fs + ((fe - fs + B - 1) / B) * B : fe;
-      while (true) {
-        const int idx = jv + lane;
-        const int x = idx < n_v ? pts[idx] : INT_MAX;
-        const bool in = x < cover;  // ascending points: a lane prefix
-        const unsigned m_in = __ballot_sync(0xffffffffu, in);
-        const bool is_col = in && x < fs;
-        const unsigned m_col = __ballot_sync(0xffffffffu, is_col);
-        if (kFill && is_col) cout[nc + __popc(m_col & lt)] = x;
-        nc += __popc(m_col);
-        jv += __popc(m_in);
-        if (m_in != 0xffffffffu) break;
+      const int cover = with_tiles ? fs + ceil_div(fe - fs) * B : fe;
+      // the next 32 points (the common case: few points per group) ...
+      const int idx = jv + lane;
+      const int x = idx < n_v ? pts[idx] : INT_MAX;
+      const bool in = x < cover;  // ascending points: a lane prefix
+      const unsigned m_in = __ballot_sync(0xffffffffu, in);
+      const bool is_col = in && x < fs;
+      const unsigned m_col = __ballot_sync(0xffffffffu, is_col);
+      if (kFill && is_col) cout[nc + __popc(m_col & lt)] = x;
+      nc += __popc(m_col);
+      jv += __popc(m_in);
+      if (m_in == 0xffffffffu) {
+        // ... then a long run: columns = the points < fs, the rest up to cover is absorbed
+        const int jc = warp_partition_point(jv, n_v, lane, [=](int p) { return pts[p] < fs; });
+        if (kFill)
+          for (int t = jv + lane; t < jc; t += 32) cout[nc + (t - jv)] = pts[t];
+        nc += jc - jv;
+        jv = warp_partition_point(jc, n_v, lane, [=](int p) { return pts[p] < cover; });
       }
       if (with_tiles) {
-        const int ntile = (fe - fs + B - 1) / B;
+        const int ntile = ceil_div(fe - fs);
         if (kFill)
           for (int t = lane; t < ntile; t += 32) tout[nt + t] = fs + t * B;
         nt += ntile;
       }
     };
     // slashes are descending: skip the prefix with o >= q_end (vs_index.py:71-72)
-    int lo = 0, hi = n_s;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sl[mid] >= q_end) lo = mid + 1;
-      else hi = mid;
-    }
+    const int lo = warp_partition_point(0, n_s, lane, [=](int j) { return sl[j] >= q_end; });
     if (lo < n_s && staged && q_end - q_start == B) {
       // full row: visit only the gap candidates after lo (the other ranges always coalesce)
       int cs = max(0, q_start - sl[lo]);
-      int g0 = 0, g1 = n_gap;
-      while (g0 < g1) {
-        const int mid = (g0 + g1) >> 1;
-        if (gaps[mid] <= lo) g0 = mid + 1;
-        else g1 = mid;
-      }
+      const int g0 = warp_partition_point(0, n_gap, lane, [=](int m) { return gaps[m] <= lo; });
       for (int base = g0; base < n_gap; base += 32) {
         const int idx = base + lane;
         const bool valid = idx < n_gap;
@@ -134,7 +163,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
           cand &= cand - 1;
           const int rs_l = __shfl_sync(0xffffffffu, rs, l);
           const int pre_l = __shfl_sync(0xffffffffu, pre, l);
-          if (rs_l >= cs + ((pre_l - cs + B - 1) / B) * B) {
+          if (rs_l >= cs + ceil_div(pre_l - cs) * B) {
             flush(cs, pre_l, true);
             cs = rs_l;
           }
@@ -157,7 +186,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) vs_merge_warp_kernel(
           cand &= cand - 1;
           const int rs_l = __shfl_sync(0xffffffffu, rs, l);
           const int pre = __shfl_sync(0xffffffffu, prev_re, l);  // current group end
-          if (rs_l >= cs + ((pre - cs + B - 1) / B) * B) {      // not coalesced (vs_index.py:78)
+          if (rs_l >= cs + ceil_div(pre - cs) * B) {  // not coalesced (vs_index.py:78)
             flush(cs, pre, true);
             cs = rs_l;
           }

@@ -41,9 +41,10 @@ constexpr int kTailRows = 64;     // last_q supported by this path
 constexpr int kMaxMembers = 4;    // q-heads per group
 constexpr int kKeys = 128;        // keys per tile (UMMA M of pass 2, N of pass 1)
 constexpr int kStages = 4;        // K tile stages
-constexpr int kThreads = 352;     // 11 warps
+constexpr int kStatWarps = 2;     // pass 1: warps taking the per-dimension max |k| of each K tile
+constexpr int kThreads = 320 + 32 * kStatWarps;  // loader, MMA, 8 epilogue warps, stat warps
 constexpr int kEpiThreads = 256;  // warps 2..9
-constexpr int kStatWarp = 10;     // pass 1: per-tile K statistics for the score error bound
+constexpr int kStatWarp = 10;     // first stat warp (pass 1: K statistics for the score error bound)
 constexpr int kGroupRows = kMaxMembers * kTailRows;
 
 struct TcArgs {
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&ctrl->q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&ctrl->k_full[s], 1);
-      mbar_init(&ctrl->k_empty[s], kPass == 1 ? 2 : 1);  // pass 1: MMA commit + K-statistics warp
+      mbar_init(&ctrl->k_empty[s], kPass == 1 ? 1 + kStatWarps : 1);  // pass 1: MMA commit + K-statistics warps
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctrl->acc_full[b], 1);
@@ -282,14 +283,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == kStatWarp) {
+  } else if (warp >= kStatWarp) {
     // ======================= K statistics (pass 1 only) =========================
     // max_j |k_jc| per dimension c over the group's keys: the input of the bound on the
-    // tensor-core score error (vs_tc_combine_kernel).  Lane l owns the 8 dims of logical
-    // 16-byte chunk (l & 15) and the keys of half (l >> 4) of every staged SW128 tile
-    // (each 128-byte row holds 64 dims of one key, chunks permuted by row & 7).
+    // tensor-core score error (vs_tc_combine_kernel).  Stat warp w takes keys
+    // [w * kKeys / kStatWarps, ...) of every staged SW128 tile; lane l owns the 8 dims of
+    // logical 16-byte chunk (l & 15) and half (l >> 4) of the warp's keys (each 128-byte row
+    // holds 64 dims of one key, chunks permuted by row & 7).
     if (kPass == 1) {
-      const int cc = lane & 15, at = cc >> 3, c = cc & 7, kh = lane >> 4;
+      constexpr int kRowsPerHalf = kKeys / kStatWarps / 2;
+      const int cc = lane & 15, at = cc >> 3, c = cc & 7;
+      const int kh = (warp - kStatWarp) * 2 + (lane >> 4);
       uint32_t amx[4] = {0u, 0u, 0u, 0u};  // |k| maxima of the lane's 8 dims, bf16x2
       for (int t = 0; t < n_tiles_cta; ++t) {
         const int st = t % kStages;
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* kst = smem + L::kOffK + st * L::kStageBytes + at * L::kKAtom;
         // keys past S are TMA zero fill: they cannot raise a maximum
 #pragma unroll 8
-        for (int r = kh * 64; r < kh * 64 + 64; ++r) {
+        for (int r = kh * kRowsPerHalf; r < (kh + 1) * kRowsPerHalf; ++r) {
           const uint4 x = *reinterpret_cast<const uint4*>(kst + r * 128 + ((c ^ (r & 7)) << 4));
           // bf16 magnitudes order like their bit patterns: per-half unsigned max
           amx[0] = __vmaxu2(amx[0], x.x & 0x7fff7fffu);
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #pragma unroll
       for (int w = 0; w < 4; ++w) amx[w] = __vmaxu2(amx[w], __shfl_xor_sync(0xffffffffu, amx[w], 16));
-      if (kh == 0 && n_tiles_cta > 0) {
+      if ((lane >> 4) == 0 && n_tiles_cta > 0) {
         uint32_t* dst = a.kabs + (int64_t)gy * kD + at * 64 + c * 8;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {

@@ -46,7 +46,7 @@ struct ExArgs {
   int S, d, L, KB, n_kblk, n_heads, hpk;
   const int32_t* head_ids;
   const int32_t* gate;     // nullable
-  const float* tile_max;   // nullable: [n_heads][64][ceil(S/128)] raw fp32 scores
+  const float* tile_max;   // nullable: [n_heads][ceil(S/128)][64] raw fp32 scores
   const float* row_mc;     // [n_heads][64]: fp32(max raw score * c)
   const float* row_marg;   // [n_heads][64]: 2 x score-error bound of the tensor-core scores (log2 units)
   float c;                 // scale * log2(e)
@@ -144,7 +144,7 @@ __device__ bool item_significant(const ExArgs& a, int h, int k0) {
   const int t = k0 / 128;
   int sig = 0;
   if (threadIdx.x < 64) {
-    const float tm = a.tile_max[((int64_t)h * 64 + threadIdx.x) * n_t + t];
+    const float tm = a.tile_max[((int64_t)h * n_t + t) * 64 + threadIdx.x];
     const float mc = a.row_mc[(int64_t)h * 64 + threadIdx.x];
     const float mg = a.row_marg[(int64_t)h * 64 + threadIdx.x];
     sig = !(tm * a.c - mc < -151.f - mg);  // NaN-safe: anything unexpected counts as significant
@@ -165,7 +165,7 @@ __global__ void vs_exact_prep_kernel(const ExArgs a) {
   const int n_t = (S + 127) / 128, t = k0 / 128;
   int sig = 0;
   for (int i = lane; i < 64; i += 32) {
-    const float tm = a.tile_max[((int64_t)h * 64 + i) * n_t + t];
+    const float tm = a.tile_max[((int64_t)h * n_t + t) * 64 + i];
     const float mc = a.row_mc[(int64_t)h * 64 + i];
     const float mg = a.row_marg[(int64_t)h * 64 + i];
     sig |= !(tm * a.c - mc < -151.f - mg);

@@ -70,7 +70,7 @@ struct TcArgs {
   double* sscore;    // [n_heads][S]  (zeroed before pass 2)
   float* tau;        // [n_heads] eta: bound on the relative error of every score-vector entry
   // for the exact fallback's tile skipping
-  float* tile_max;   // [n_heads][64][n_tiles] raw row max per 128-key tile
+  float* tile_max;   // [n_heads][n_tiles][64] raw row max per 128-key tile (rows fastest)
   float* row_mc;     // [n_heads][64] mc per slot
   uint8_t* live;     // [groups][n_tiles] pass-2 tile holds a probability that is not flushed to 0
 };
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[j] = ok ? x[j] : 0xf149f2cau;  // -1e30 (finite): 2^(y) underflows to 0
             }
           }
-          a.tile_max[((int64_t)ctrl->slot[mm] * kTailRows + i) * a.n_tiles + tile] = tmax;
+          a.tile_max[((int64_t)ctrl->slot[mm] * a.n_tiles + tile) * kTailRows + i] = tmax;
           // every exponent of this row below the flush threshold: the tile adds exactly 0
           const bool dead = n_valid <= 0 || (m_run != -INFINITY && tmax <= m_run && fmaf(tmax, c, -mc_run) < kDeadExp);
           const bool warp_dead = __all_sync(0xffffffffu, dead);
@@ -628,17 +628,21 @@ __global__ void __launch_bounds__(256) vs_tc_live_kernel(const TcArgs a) {
   __syncthreads();
   const int nh = nh_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
-  if (t < a.n_tiles) {
+  // warp w: tiles 4w .. 4w+3 of the CTA's 32; lanes read 32 consecutive rows (coalesced)
+  for (int u = 4 * w; u < 4 * w + 4; ++u) {
+    const int tu = blockIdx.x * 32 + u;
+    if (tu >= a.n_tiles) break;
     bool live = false;
-    for (int r = w; r < nh * kTailRows && !live; r += 8) {
+    for (int r = lane; r < nh * kTailRows; r += 32) {
       const int mm = r / kTailRows, i = r % kTailRows;
-      const int64_t row = (int64_t)slot[mm] * kTailRows + i;
-      live = fmaf(a.tile_max[row * a.n_tiles + t], a.c_hi, -a.row_mc[row]) >= kDeadExp;
+      live |= fmaf(a.tile_max[((int64_t)slot[mm] * a.n_tiles + tu) * kTailRows + i], a.c_hi,
+                   -a.row_mc[(int64_t)slot[mm] * kTailRows + i]) >= kDeadExp;
     }
-    if (live) lv[lane] = 1;
+    const bool any = __any_sync(0xffffffffu, live);
+    if (lane == 0) lv[u] = any ? 1 : 0;
   }
   __syncthreads();
+  const int t = blockIdx.x * 32 + lane;
   if (threadIdx.x < 32 && t < a.n_tiles) a.live[(int64_t)gy * a.n_tiles + t] = (uint8_t)lv[threadIdx.x];
   for (int u = 0; u < 32; ++u) {  // zero the vertical scores of the dead tiles (coalesced)
     const int tu = blockIdx.x * 32 + u;

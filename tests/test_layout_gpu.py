@@ -86,12 +86,14 @@ def test_large_merge_matches_c_oracle(P, rng):
     np.testing.assert_array_equal(c, wc)
 
 
-@pytest.mark.parametrize("kind", ["band", "spaced_b", "spaced_b1", "clustered"])
+@pytest.mark.parametrize("kind", ["band", "spaced_b", "spaced_b1", "clustered", "dense_v", "unstaged"])
 def test_structured_merges_match_c_oracle(P, rng, kind):
     """Slash patterns that stress the coalescing rule of the warp-parallel
     merge: one contiguous band (G-local), offsets exactly B and B+1 apart
     (every range a gap candidate, half of them coalesced by the cover rule),
-    and clustered offsets."""
+    and clustered offsets; dense verticals (groups absorbing and rows emitting
+    hundreds of points: the warp-wide partition searches) with the lists staged
+    in shared memory and, past its capacity, read from global memory."""
     s_len, b = 65536 + 37, 64
     if kind == "band":
         slash = np.arange(6095, -1, -1)
@@ -99,11 +101,16 @@ def test_structured_merges_match_c_oracle(P, rng, kind):
         slash = np.arange(0, 64 * 900, 64)[::-1]
     elif kind == "spaced_b1":
         slash = np.arange(0, 65 * 900, 65)[::-1]
-    else:
+    elif kind == "clustered":
         centers = rng.choice(s_len - 200, size=60, replace=False)
         slash = np.unique((centers[:, None] + rng.integers(0, 150, size=(60, 40))).ravel())[::-1]
+    elif kind == "dense_v":
+        slash = np.arange(6095, -1, -1)
+    else:  # unstaged: n_v + 2 n_s above the shared-memory capacity (24K indices)
+        slash = np.sort(rng.choice(s_len, size=8000, replace=False))[::-1]
     slash = slash[slash < s_len]
-    vertical = np.sort(rng.choice(s_len, size=1000, replace=False))
+    n_v = {"dense_v": 6000, "unstaged": 10000}.get(kind, 1000)
+    vertical = np.sort(rng.choice(s_len, size=n_v, replace=False))
     layout = P.build_vs_layout(P.VSIndices(vertical=vertical, slash=slash), s_len, b)
     t, to, c, co = layout.csr()
     wt, wto, wc, wco = port.build_vs_csr(vertical, slash, s_len, b)

@@ -119,17 +119,6 @@ struct Layout {
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
-// D[tmem] (+)= A[tmem] * B[smem]: P (bf16, K-major, 2 per 32-bit column) times V.
-__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
 // One step of the loader's schedule.
 struct StepInfo {
   int kind;

@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_q2,
                            const __grid_constant__ CUtensorMap tm_k2, const __grid_constant__ CUtensorMap tm_v2,
-                           const AttnArgs p, int n_ctile, float scale_log2) {
+                           const __grid_constant__ CUtensorMap tm_o, const AttnArgs p, int n_ctile,
+                           float scale_log2) {
   using L = Layout<kD, kSplit>;
   using R = Rings<kSplit>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -732,7 +733,43 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
     }
     if (p.lse != nullptr && half == 0 && q < S)
       p.lse[(int64_t)h * S + q] = (t > 0 && l_tot > 0.f) ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
-    {
+    if (!kSplit && kHalves == 1 && !p.out_f32 && p.d_out == kD) {
+      // O / l as bf16 into the (now idle) K ring in the SW128 layout of a TMA tile -- 16-byte
+      // chunk c of row r at c ^ (r & 7) -- then one tensor store per 64-column atom (rows
+      // past S clipped by the map): coalesced, where per-row stores touch one sector per lane
+      const float inv = (t > 0 && l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      uint8_t* ost = smem + L::kOffK;  // every MMA, load and gather into the rings has retired
+#pragma unroll
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t o[32];
+        __syncwarp();
+        if (t > 0) {
+          tmem_ld32x32b_x32(tmem + lane_off + 128 + c, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = 0u;
+        }
+        const uint32_t rbase = smem_u32(ost) + (uint32_t)((c >> 6) * (kRows * 128) + row * 128);
+        const int ch0 = (c & 63) >> 3;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int j = 8 * k4;
+          st_shared_v4(rbase + ((((ch0 + k4) ^ (row & 7))) << 4), pack_bf16x2(u2f(o[j]) * inv, u2f(o[j + 1]) * inv),
+                       pack_bf16x2(u2f(o[j + 2]) * inv, u2f(o[j + 3]) * inv),
+                       pack_bf16x2(u2f(o[j + 4]) * inv, u2f(o[j + 5]) * inv),
+                       pack_bf16x2(u2f(o[j + 6]) * inv, u2f(o[j + 7]) * inv));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (threadIdx.x == 64) {
+#pragma unroll
+        for (int a = 0; a < L::kAtoms; ++a) tma_store_3d(&tm_o, ost + a * (kRows * 128), a * 64, R0, h);
+        bulk_commit_group();
+        bulk_wait_group0();
+      }
+    } else {
       const float inv = (t > 0 && l_tot > 0.f) ? 1.f / l_tot : 0.f;
       const int dout = p.d_out;
       const int64_t obase = ((int64_t)h * S + min(q, S - 1)) * dout + oc0;
@@ -791,7 +828,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
 template <int kD, bool kSplit>
 int launch_impl(const AttnArgs& a, cudaStream_t stream) {
   using L = Layout<kD, kSplit>;
-  CUtensorMap tq, tk, tv, tq2, tk2, tv2;
+  CUtensorMap tq, tk, tv, tq2, tk2, tv2, to;
   int rc;
   if ((rc = make_tmap_bf16_3d(&tq, a.q_hi, kD, a.S, a.Hq, kRows))) return rc;
   if ((rc = make_tmap_bf16_3d(&tk, a.k_hi, kD, a.S, a.Hkv, kBox))) return rc;
@@ -804,6 +841,12 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
     tq2 = tq;
     tk2 = tk;
     tv2 = tv;
+  }
+  // bf16 output of the padded width: stored by tensor-map tiles (see the epilogue)
+  if (!kSplit && !a.out_f32 && a.d_out == kD) {
+    if ((rc = make_tmap_bf16_3d(&to, a.out, kD, a.S, a.Hq, kRows))) return rc;
+  } else {
+    to = tq;
   }
   auto kern = sparse_attn_fwd_kernel<kD, kSplit>;
   constexpr int kLaunchSmem = L::kSmem;
@@ -819,7 +862,7 @@ int launch_impl(const AttnArgs& a, cudaStream_t stream) {
   if (grid > 0x7fffffffLL) return set_error(2, "attention grid too large");
   const float scale_log2 = a.scale * 1.4426950408889634f;
   note_launches(1);
-  kern<<<(unsigned)grid, kThreadsT<kSplit>, kLaunchSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, a, n_ctile, scale_log2);
+  kern<<<(unsigned)grid, kThreadsT<kSplit>, kLaunchSmem, stream>>>(tq, tk, tv, tq2, tk2, tv2, to, a, n_ctile, scale_log2);
   return check_cuda(cudaGetLastError(), "sparse_attn_fwd launch");
 }
 

@@ -402,7 +402,10 @@ __device__ __forceinline__ void fb_store(__nv_bfloat16* dst, const int4 (&r)[kD 
 
 __device__ __forceinline__ double bf16_to_f64(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
 
-// acc[mi][ni] = 8x8 tiles of Q K^T: rows m0 + 8 mi (+ lane / 4), keys n0 + 8 ni (+ 2 (lane % 4) + {0, 1})
+// acc[mi][ni] = 8x8 tiles of Q K^T: rows m0 + 8 mi (+ lane / 4), keys n0 + 8 ni (+ 2 (lane % 4) + {0, 1}).
+// The k4 steps of the DMMA walk each 16-wide slice of d as k = 16 kk + 4 (lane % 4) + j for
+// j = 0..3 (the same map for both operands, so every k of the slice is summed once): each
+// lane's four values of a slice are contiguous, one 8-byte load per fragment per 4 DMMAs.
 template <int kD>
 __device__ __forceinline__ void fb_scores(const __nv_bfloat16* Qs, const __nv_bfloat16* Ks, int m0, int n0,
                                           double (&acc)[2][4][2]) {
@@ -412,19 +415,33 @@ __device__ __forceinline__ void fb_scores(const __nv_bfloat16* Qs, const __nv_bf
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  const __nv_bfloat16* qa = Qs + (m0 + (lane >> 2)) * kLd + (lane & 3);
-  const __nv_bfloat16* kb = Ks + (n0 + (lane >> 2)) * kLd + (lane & 3);
-#pragma unroll 8
-  for (int ks = 0; ks < kD / 4; ++ks) {
-    double a[2], b[4];
+  const __nv_bfloat16* qa = Qs + (m0 + (lane >> 2)) * kLd + 4 * (lane & 3);
+  const __nv_bfloat16* kb = Ks + (n0 + (lane >> 2)) * kLd + 4 * (lane & 3);
+#pragma unroll 2
+  for (int kk = 0; kk < kD / 16; ++kk) {
+    uint2 ar[2], br[4];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) a[mi] = bf16_to_f64(qa[mi * 8 * kLd + 4 * ks]);
+    for (int mi = 0; mi < 2; ++mi) ar[mi] = *reinterpret_cast<const uint2*>(qa + mi * 8 * kLd + 16 * kk);
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = bf16_to_f64(kb[ni * 8 * kLd + 4 * ks]);
+    for (int ni = 0; ni < 4; ++ni) br[ni] = *reinterpret_cast<const uint2*>(kb + ni * 8 * kLd + 16 * kk);
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int j = 0; j < 4; ++j) {
+      double a[2], b[4];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma_f64(acc[mi][ni], a[mi], b[ni]);
+      for (int mi = 0; mi < 2; ++mi) {
+        const uint32_t w = j < 2 ? ar[mi].x : ar[mi].y;
+        a[mi] = (double)__uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16));
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const uint32_t w = j < 2 ? br[ni].x : br[ni].y;
+        b[ni] = (double)__uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16));
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_f64(acc[mi][ni], a[mi], b[ni]);
+    }
   }
 }
 

@@ -231,22 +231,34 @@ __global__ void __launch_bounds__(kScoreDmmaThreads, 3) bs_score_dmma_kernel(
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 8; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  const float* qa = As + (16 * warp + (lane >> 2)) * kLd + (lane & 3);
-  const float* kb = Bs + (lane >> 2) * kLd + (lane & 3);
-#pragma unroll 4
-  for (int ks = 0; ks < kD / 4; ++ks) {
-    double a[2], b[8];
+  // k4 steps walk each 16-wide slice of d as k = 16 kk + 4 (lane % 4) + j, j = 0..3 (the same
+  // map for both operands): a lane's four values of a slice are one 16-byte load
+  const float* qa = As + (16 * warp + (lane >> 2)) * kLd + 4 * (lane & 3);
+  const float* kb = Bs + (lane >> 2) * kLd + 4 * (lane & 3);
+#pragma unroll 1
+  for (int kk = 0; kk < kD / 16; ++kk) {
+    float4 af[2], bf[8];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) a[mi] = (double)qa[mi * 8 * kLd + 4 * ks];
+    for (int mi = 0; mi < 2; ++mi) af[mi] = *reinterpret_cast<const float4*>(qa + mi * 8 * kLd + 16 * kk);
 #pragma unroll
-    for (int ni = 0; ni < 8; ++ni) b[ni] = (double)kb[ni * 8 * kLd + 4 * ks];
+    for (int ni = 0; ni < 8; ++ni) bf[ni] = *reinterpret_cast<const float4*>(kb + ni * 8 * kLd + 16 * kk);
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int j = 0; j < 4; ++j) {
+      double a[2], b[8];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+        a[mi] = (double)(j == 0 ? af[mi].x : j == 1 ? af[mi].y : j == 2 ? af[mi].z : af[mi].w);
 #pragma unroll
       for (int ni = 0; ni < 8; ++ni)
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
-                     : "d"(a[mi]), "d"(b[ni]));
+        b[ni] = (double)(j == 0 ? bf[ni].x : j == 1 ? bf[ni].y : j == 2 ? bf[ni].z : bf[ni].w);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+                       : "d"(a[mi]), "d"(b[ni]));
+    }
   }
   double* outh = out + (int64_t)hi * N * N;
 #pragma unroll

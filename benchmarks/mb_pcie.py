@@ -38,3 +38,37 @@ def both():
 
 t = timed(both)
 print("H2D + D2H concurrent: %.1f GB/s each direction" % (n / t / 1e6))
+
+
+# two H2D streams (two copy engines) against one D2H: does a second engine raise the
+# aggregate when both directions run?
+s3 = torch.cuda.Stream()
+half = n // 2
+
+
+def both2():
+    with torch.cuda.stream(s1):
+        d[:half].copy_(h[:half], non_blocking=True)
+    with torch.cuda.stream(s3):
+        d[half:].copy_(h[half:], non_blocking=True)
+    with torch.cuda.stream(s2):
+        h2.copy_(d2, non_blocking=True)
+    for s in (s1, s2, s3):
+        torch.cuda.current_stream().wait_stream(s)
+
+
+t = timed(both2)
+print("2x H2D (halves) + D2H concurrent: %.1f GB/s each direction" % (n / t / 1e6))
+
+
+def h2d2():
+    with torch.cuda.stream(s1):
+        d[:half].copy_(h[:half], non_blocking=True)
+    with torch.cuda.stream(s3):
+        d[half:].copy_(h[half:], non_blocking=True)
+    for s in (s1, s3):
+        torch.cuda.current_stream().wait_stream(s)
+
+
+t = timed(h2d2)
+print("2x H2D (halves) alone: %.1f GB/s" % (n / t / 1e6))

@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
 #pragma unroll
         for (int a = 0; a < L::kAtoms; ++a) tma_store_3d(&tm_o, ost + a * (kRows * 128), a * 64, R0, h);
         bulk_commit_group();
-        bulk_wait_group0();
+        bulk_wait_group_read0();
       }
     } else {
       const float inv = (t > 0 && l_tot > 0.f) ? 1.f / l_tot : 0.f;

@@ -113,20 +113,27 @@ struct TcLayout {
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
 // Members of group gy: the (4*sub .. 4*sub+3)-th slots (ascending) whose head maps to kv head gy / gpk.
+// Group gy's members (q-heads of one kv head, at most kMaxMembers, in list order): slot = index
+// in the head list, head = q-head id.  Called by a whole warp: 32 list entries per round with
+// a ballot (one serial pass of dependent loads per entry cost ~10 us per CTA); lane 0 stores.
 __device__ int group_members(const TcArgs& a, int gy, int* slot, int* head) {
+  const int lane = threadIdx.x & 31;
   const int kvh = gy / a.gpk, sub = gy % a.gpk;
-  int seen = 0, nh = 0;
-  for (int i = 0; i < a.n_heads; ++i) {
-    const int h = a.head_ids ? a.head_ids[i] : i;
-    if (h / a.hpk != kvh) continue;
-    if (seen >= kMaxMembers * sub && seen < kMaxMembers * (sub + 1)) {
-      slot[nh] = i;
-      head[nh] = h;
-      ++nh;
+  const int lo = kMaxMembers * sub, hi = kMaxMembers * (sub + 1);
+  int seen = 0;
+  for (int base = 0; base < a.n_heads; base += 32) {
+    const int i = base + lane;
+    const int h = i < a.n_heads ? (a.head_ids ? a.head_ids[i] : i) : -1;
+    const bool match = h >= 0 && h / a.hpk == kvh;
+    const unsigned m = __ballot_sync(0xffffffffu, match);
+    const int rank = seen + __popc(m & ((1u << lane) - 1u));
+    if (match && rank >= lo && rank < hi) {
+      slot[rank - lo] = i;
+      head[rank - lo] = h;
     }
-    ++seen;
+    seen += __popc(m);
   }
-  return nh;
+  return min(kMaxMembers, max(0, seen - lo));
 }
 
 template <int kD, int kPass>
@@ -143,8 +150,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_end = (int)((int64_t)(chunk + 1) * a.n_tiles / a.n_chunks);
   const int kvh = gy / a.gpk;
 
+  if (warp == 0) {
+    const int nh = group_members(a, gy, ctrl->slot, ctrl->head);
+    if (lane == 0) ctrl->nh = nh;
+  }
   if (threadIdx.x == 0) {
-    ctrl->nh = group_members(a, gy, ctrl->slot, ctrl->head);
     if ((sbase & 1023u) != 0) {
       printf("spf: dynamic smem not 1024-aligned\n");
       __trap();
@@ -548,7 +558,10 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
   __shared__ float err_s[kGroupRows];
   __shared__ float kabs_s[kD];
   const int gy = blockIdx.x;
-  if (threadIdx.x == 0) nh_s = group_members(a, gy, slot, head);
+  if (threadIdx.x < 32) {
+    const int n = group_members(a, gy, slot, head);
+    if (threadIdx.x == 0) nh_s = n;
+  }
   for (int c = threadIdx.x; c < kD; c += blockDim.x)
     kabs_s[c] = __uint_as_float(a.kabs[(int64_t)gy * kD + c] << 16);
   __syncthreads();
@@ -559,11 +572,14 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
   float amax = 0.f, err = 0.f;
   if (mm < nh) {
     float m = -INFINITY;
+    // unrolled: the chunk partials' loads are independent (one round trip per 8, not per chunk)
+#pragma unroll 8
     for (int c = 0; c < a.n_chunks; ++c) {
       const int64_t o = ((int64_t)gy * a.n_chunks + c) * kGroupRows + r;
       if (a.st_l[o] > 0.0) m = fmaxf(m, a.st_m[o]);
     }
     double l = 0.0;  // st_m holds mc = fp32(m * c): rescale in the exponent domain the sums were taken in
+#pragma unroll 8
     for (int c = 0; c < a.n_chunks; ++c) {
       const int64_t o = ((int64_t)gy * a.n_chunks + c) * kGroupRows + r;
       const double lc = a.st_l[o];
@@ -601,6 +617,7 @@ __global__ void __launch_bounds__(kGroupRows) vs_tc_combine_kernel(const TcArgs 
   __syncthreads();
   if (r < nh) {
     float mx = 0.f, emax = 0.f;
+#pragma unroll 16
     for (int i = 0; i < kTailRows; ++i) {
       mx = fmaxf(mx, amax_s[r * kTailRows + i]);
       emax = fmaxf(emax, err_s[r * kTailRows + i]);
@@ -623,7 +640,10 @@ __global__ void __launch_bounds__(256) vs_tc_live_kernel(const TcArgs a) {
   __shared__ int slot[kMaxMembers], head[kMaxMembers], nh_s;
   __shared__ int lv[32];
   const int gy = blockIdx.y;
-  if (threadIdx.x == 0) nh_s = group_members(a, gy, slot, head);
+  if (threadIdx.x < 32) {
+    const int n = group_members(a, gy, slot, head);
+    if (threadIdx.x == 0) nh_s = n;
+  }
   if (threadIdx.x < 32) lv[threadIdx.x] = 0;
   __syncthreads();
   const int nh = nh_s;

@@ -153,11 +153,16 @@ __global__ void __launch_bounds__(kThreadsT<kSplit>, kSplit ? 1 : 2)
   const int ct = n_ctile - 1 - item / p.Hq;
   const int h = item % p.Hq;
   const int kvh = h / (p.Hq / p.Hkv);
-  for (int i = 0; i < p.n_pair; ++i)
-    if (p.pair_heads[i] == h) {
-      if (pair_preferred(p.pair_stats, i)) return;  // run by the paired-box kernel (attn_bs.cu)
+  // routed to the paired-box kernel (attn_bs.cu)?  The first listed entry of this head decides;
+  // every warp scans the list 32 entries per ballot (the same answer in all warps)
+  for (int base = 0; base < p.n_pair; base += 32) {
+    const int i = base + (threadIdx.x & 31);
+    const unsigned m = __ballot_sync(0xffffffffu, i < p.n_pair && p.pair_heads[i] == h);
+    if (m) {
+      if (pair_preferred(p.pair_stats, base + __ffs(m) - 1)) return;
       break;
     }
+  }
   const int S = p.S, B = p.B;
   const int n_rows = (S + B - 1) / B;
   const int R0 = ct * kRows;

@@ -458,13 +458,21 @@ __global__ void __launch_bounds__(kFbThreads, 2) vs_fb_kernel(const __nv_bfloat1
   int* off = reinterpret_cast<int*>(smraw + SM::kOffOff);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = a.S, nh = a.n_heads;
-  if (tid == 0) {  // virtual item offsets of the heads' lists
+  if (warp == 0) {  // virtual item offsets of the heads' lists: a warp prefix sum, 32 heads per round
     int o = 0;
-    for (int h = 0; h < nh; ++h) {
-      off[h] = o;
-      o += (a.gate != nullptr && a.gate[h] == 0) ? 0 : a.head_count[h];
+    for (int base = 0; base < nh; base += 32) {
+      const int h = base + lane;
+      const int c = h < nh ? ((a.gate != nullptr && a.gate[h] == 0) ? 0 : a.head_count[h]) : 0;
+      int incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      if (h < nh) off[h] = o + incl - c;
+      o += __shfl_sync(0xffffffffu, incl, 31);
     }
-    off[nh] = o;
+    if (lane == 0) off[nh] = o;
   }
   __syncthreads();
   const int total = off[nh];

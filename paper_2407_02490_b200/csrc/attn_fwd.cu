@@ -9,18 +9,21 @@
 //     query being the leading columns <= query (_core.pyx:172-179);
 //   * one streaming-softmax state per query row; out = acc / l, zero row if l == 0.
 //
-// B200 design (DESIGN.md section 3):
-//   * one CTA = 128 query rows of one q-head (UMMA M = 128).  The row blocks
-//     it covers (2 when B = 64) are merged into one union step list; each step
+// B200 design (DESIGN.md section 4):
+//   * one CTA = 128 query rows of one q-head (UMMA M = 128), two CTAs per SM.  The row
+//     blocks it covers (2 when B = 64) are merged into one union step list; each step
 //     carries a segment mask so a row block never sees another block's keys.
-//   * step = 64 keys: a TMA-loaded box of K/V (tiles) or a warp-gathered chip
-//     of K/V rows (columns), double-buffered in shared memory;
-//   * S = Q K^T   : tcgen05.mma M128 N64 K=d, fp32 accumulator in TMEM
-//                   (two S buffers so QK(t+1) overlaps softmax(t));
-//   * O += P V    : tcgen05.mma M128 N=d K64, P bf16 in SW128 smem, V MN-major,
-//                   fp32 accumulator resident in TMEM for the whole row tile;
+//   * step = 64 keys: a TMA-loaded box of K/V (tiles) or a cp.async-gathered chip of
+//     K/V rows (columns), in 3-deep K / 2-deep V rings in shared memory;
+//   * S = Q K^T   : tcgen05.mma M128 N64 K=d, fp32 accumulator in TMEM columns [0,64),
+//                   released as soon as the softmax has read it so QK(t+1) overlaps
+//                   softmax(t);
+//   * O += P V    : tcgen05.mma M128 N=d K64 with A = P (bf16, its own double-buffered
+//                   TMEM columns [64,128)), V MN-major from shared memory, fp32 O resident
+//                   in TMEM [128,256) for the whole row tile; the epilogue stages O / l in
+//                   the idle K ring and writes it with tensor-map stores;
 //   * warp roles: warp0 = loader (TMA + gathers + union merge), warp1 = MMA
-//     issuer (one thread) + TMEM owner, warps2-5 = softmax (thread <-> row).
+//     issuer (elected lane) + TMEM owner, warps2-5 = softmax (thread <-> row).
 //   * online softmax in the exp2 domain with lazy rescaling (only when the
 //     running max grows by > 8, i.e. p <= 256); results are identical up to
 //     rounding to the reference's exact-max recurrence.

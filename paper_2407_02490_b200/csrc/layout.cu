@@ -2,13 +2,13 @@
 // layouts for the three patterns, plus the CSR scan and the layout-area
 // accounting.  Integer work, bit-exact with the reference.
 //
-//  * Vertical-Slash point-range merge (Alg. 4), vs_index.py:28-95: one thread
-//    per query-block row walks the head's slash offsets (descending) as ranges
-//    and its verticals (ascending) as points; count pass -> scan -> fill pass.
+//  * Vertical-Slash point-range merge (Alg. 4), vs_index.py:28-95: one warp per
+//    query-block row walks the head's slash offsets (descending) as ranges and its
+//    verticals (ascending) as points; count pass -> scan -> fill pass.
 //  * A-shape, patterns.py:109-128: aligned sink tiles below the local window
 //    start, then the aligned local window.
 //  * Block-Sparse row counts min(k_b, r+1) (estimator.py:139-142); the tile
-//    entries themselves are written by the BS estimator (estimate_bs.cu).
+//    entries themselves are written by the BS estimator (estimate.cu).
 //  * layout_area, patterns.py:147-184 (diagonal tile clipped to its lower
 //    triangle, column chips rounded up to B).
 #include <cub/block/block_scan.cuh>

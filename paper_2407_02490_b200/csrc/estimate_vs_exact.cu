@@ -400,7 +400,6 @@ __device__ __forceinline__ void fb_store(__nv_bfloat16* dst, const int4 (&r)[kD 
   }
 }
 
-__device__ __forceinline__ double bf16_to_f64(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
 
 // acc[mi][ni] = 8x8 tiles of Q K^T: rows m0 + 8 mi (+ lane / 4), keys n0 + 8 ni (+ 2 (lane % 4) + {0, 1}).
 // The k4 steps of the DMMA walk each 16-wide slice of d as k = 16 kk + 4 (lane % 4) + j for

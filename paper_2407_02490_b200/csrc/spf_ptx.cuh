@@ -32,9 +32,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// No suspend-time hint: with one (10 ms) a waiting warp is parked and woken later than the
-// phase completes -- 2.7 % on the union attention kernel's barrier chain and 6.6 % on the
-// paired-box kernel (interleaved A/B); mbarrier.test_wait spinning measured no better.
+// No suspend-time hint: with one (10 ms, and even 256 ns) a waiting warp is parked and woken
+// later than the phase completes -- 2.7-5 % on the union attention kernel's barrier chain and
+// 6.6-7 % on the paired-box kernel (interleaved A/B); mbarrier.test_wait spinning no better.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(

@@ -139,8 +139,11 @@ def run_reference_arm(args, cfg):
             "sample_items_per_step": info["items"],
             "metric": metric_name(args, cfg), "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 3), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 storage)", "data": "synthetic (G-local)",
-            "config": {"workload": cfg["workload"], "seq_len": cfg["seq_len"], "layers": cfg["layers"]},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 storage)", "data": "synthetic",
+            # the workload identity keys of the GPU arm's config (same workload, shapes and patterns)
+            "config": {"workload": cfg["workload"], "seq_len": cfg["seq_len"], "layers": cfg["layers"],
+                       "q_heads": cfg["hq"], "kv_heads": cfg["hkv"], "head_dim": 128, "block_size": 64,
+                       "patterns": cfg["patterns"], "inputs": cfg["inputs"] + " (SURVEY.md 8d)"},
             "cpu_baseline": {"value": round(value, 3), "unit": "ms", "cores": cores, "kind": "reference"
                              if info["ref_kernel"] else "port", "sample": sample},
             "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
